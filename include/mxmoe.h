@@ -1,0 +1,145 @@
+/* mxmoe.h — C ABI of the B200-native MxMoE mixed-precision MoE group-GEMM.
+ *
+ * The operations follow the paper's statement of the problem (arXiv 2505.05799,
+ * /root/reference/PAPER.md, cited "P:<line>"):
+ *   - uniform min-max quantization of a linear block (§2.1) at a per-block
+ *     bit-width / group size / symmetry (per-linear-block allocation, §4.2.1);
+ *   - a mixed-precision Group-GEMM that runs every expert's gate/up/down linear block,
+ *     each at its own precision, over the routed token groups (§2.2, §4.3),
+ *     computing the MoE block F = Σ_e W_down^e(σ(W_gate^e X_e) ⊙ W_up^e X_e) ⊙ w_e
+ *     (Eq. 1, Eq. 2), with activations quantized dynamically at runtime
+ *     for weight-activation schemes.
+ * Exact numerical definitions (rounding, scale round-up, fp32 activation quantizer)
+ * are the readings listed in DESIGN.md §2.
+ *
+ * Conventions (all entry points):
+ *   - Tensor pointers are CUDA DEVICE pointers OWNED BY THE CALLER unless the parameter
+ *     says "host". The library never allocates device memory and never frees caller memory.
+ *   - Calls marked [async] enqueue work on `stream` and return without synchronizing;
+ *     [sync] calls may block the host.
+ *   - Errors are returned, never thrown: MXM_E_CONFIG (unsupported scheme/shape; nothing is
+ *     launched), MXM_E_DATA (bad data detected on device; surfaced by mxm_poll_device_error),
+ *     MXM_E_CUDA (a CUDA call failed; see mxm_last_error()).
+ *   - Row-major layouts; bf16 is IEEE bfloat16 bit patterns (uint16).
+ */
+#ifndef MXMOE_H
+#define MXMOE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { MXM_OK = 0, MXM_E_CONFIG = 3, MXM_E_DATA = 4, MXM_E_CUDA = 5, MXM_E_NCCL = 6 } mxm_status;
+
+/* Quantization scheme `wxay_gz_{sym,asym}` (PAPER.md P:92 caption of fig:motivation).
+ *   w_bits    2,3,4,8 (weight-only) | 4,5,8 (weight-activation) | 16 (bf16 pass-through)
+ *   a_bits    16 = weight-only; otherwise == w_bits (w4a4, w5a5, w8a8)
+ *   w_group   -1 = per-channel, else 64 or 128 (weight-only), 128 (weight-activation); divides K
+ *   a_group   weight-activation: == w_group (-1 = per-token); weight-only: ignored
+ *   symmetric 1 = scale only; 0 = scale + zero-point (weight-only only)                        */
+typedef struct {
+  int32_t w_bits, a_bits, w_group, a_group, symmetric;
+} mxm_scheme;
+
+typedef void* mxm_stream; /* a cudaStream_t */
+
+enum { MXM_GATE = 0, MXM_UP = 1, MXM_DOWN = 2 };
+
+/* ---------------------------------------------------------------- metadata [sync, host only] */
+/* MXM_OK if the scheme is supported for a block W[N, K]; MXM_E_CONFIG otherwise. */
+mxm_status mxm_scheme_check(const mxm_scheme* s, int64_t N, int64_t K);
+/* Sizes in bytes of the canonical quantizer outputs and of the packed buffer (docs/packed_format.md). */
+mxm_status mxm_quant_sizes(const mxm_scheme* s, int64_t N, int64_t K, int64_t* codes_bytes, int64_t* scale_bytes,
+                           int64_t* zero_bytes, int64_t* packed_bytes);
+/* w + (1 sym | 2 asym)·16/g with g = K for per-channel (3.25 / 2.25 for w3/w2-g128-asym). */
+double mxm_storage_bits_per_weight(const mxm_scheme* s, int64_t K);
+
+/* ---------------------------------------------------------------- setup [async]
+ * Quantize W[N, K] (bf16, K contiguous) group-wise along K with the min-max rule:
+ *   codes  [N, K] uint8 (asym, q in [0, 2^b-1]) or int8 (sym, |q| <= 2^(b-1)-1)
+ *   scale  [N, K/g] bf16, the smallest bf16 s with (2^b-1)s >= max-min (asym) or (2^(b-1)-1)s >= max|x|
+ *   zero   [N, K/g] bf16 = group min (asym); may be NULL when symmetric
+ * fp64 arithmetic; results are bit-exact with the CPU oracle. w_bits = 16 is rejected (nothing to quantize).
+ * A non-finite weight sets the device error word (MXM_E_DATA) if `err` is non-NULL (int32, device). */
+mxm_status mxm_quantize(const mxm_scheme* s, const void* w_bf16, int64_t N, int64_t K, void* codes, void* scale,
+                        void* zero, int32_t* err, mxm_stream stream);
+/* Pack canonical codes/scale/zero into the native layout (docs/packed_format.md); `packed` has
+ * mxm_quant_sizes(...).packed_bytes bytes. For w_bits = 16, `codes` is the bf16 weight and
+ * scale/zero are ignored. */
+mxm_status mxm_pack(const mxm_scheme* s, const void* codes, const void* scale, const void* zero, int64_t N, int64_t K,
+                    void* packed, mxm_stream stream);
+/* Test/debug: dequantize a packed block to float32 w_out[N, K] = q·s + z exactly (q·s sym). */
+mxm_status mxm_dequantize(const mxm_scheme* s, const void* packed, int64_t N, int64_t K, float* w_out,
+                          mxm_stream stream);
+
+/* Test/debug: the dynamic activation quantizer of the hot path on v[M, K] bf16:
+ *   codes [M, K] int8, scale [M, K/ga] float32, qsum [M, K/ga] int32 (may be NULL).
+ *   r = fl32(qmax/amax), s = fl32(amax/qmax), q = clamp(rint(fl32(v·r)), ±qmax); amax = 0 -> s = 1, q = 0. */
+mxm_status mxm_act_quant(const void* v_bf16, int64_t M, int64_t K, int32_t a_bits, int32_t a_group, void* codes,
+                         float* scale, int32_t* qsum, mxm_stream stream);
+
+/* Test/debug: the hot path's route preparation (step S1). topk_ids int32[T, k] (-1 = none).
+ *   counts  int32[E]      routes per expert
+ *   offsets int32[E + 1]  exclusive scan of counts
+ *   perm    int32[T*k]    perm[p] = t*k + j of the route at sorted position p (stable in (t, j) order);
+ *                         entries >= offsets[E] are left untouched
+ *   err     int32 device word, set to MXM_E_DATA for an id outside [-1, E) (that route is skipped) */
+mxm_status mxm_route_prep(const int32_t* topk_ids, int64_t T, int32_t k, int32_t E, int32_t* counts,
+                          int32_t* offsets, int32_t* perm, int32_t* err, void* scratch, int64_t scratch_bytes,
+                          mxm_stream stream);
+
+/* ---------------------------------------------------------------- layer (the per-block precision table)
+ * blocks: host array [(n_routed + n_shared) * 3], order (expert-major) gate, up, down; gate/up are [inter, hidden]
+ * (routed) or [shared_inter, hidden] (shared); down is [hidden, inter]. `packed` are device buffers from mxm_pack,
+ * which must stay alive while the layer is used. Shared experts see every token (weight shared_w or 1). */
+typedef struct {
+  mxm_scheme scheme;
+  const void* packed;
+} mxm_linear;
+typedef struct {
+  int32_t n_routed, n_shared, hidden, inter, shared_inter;
+  const mxm_linear* blocks;
+} mxm_layer_desc;
+typedef struct mxm_layer mxm_layer;
+
+/* [sync] device bytes needed for the layer's descriptor table. */
+mxm_status mxm_layer_desc_bytes(const mxm_layer_desc* d, int64_t* bytes);
+/* [sync] validate every block, upload the descriptor table into desc_dev (caller-owned device buffer of
+ * mxm_layer_desc_bytes bytes), return a host handle. tile_costs: NULL = analytic LPT cost model. */
+mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_bytes, const void* tile_costs,
+                          mxm_layer** out);
+void mxm_layer_free(mxm_layer* l);
+/* [sync] workspace bytes for calls with up to max_tokens tokens and top_k routes per token. */
+mxm_status mxm_workspace_bytes(const mxm_layer* l, int64_t max_tokens, int32_t top_k, int64_t* bytes);
+
+/* [async] The mixed-precision MoE group-GEMM (the hot path):
+ *   x        bf16 [T, hidden]
+ *   topk_ids int32 [T, top_k], -1 = no route; duplicates allowed (each contributes)
+ *   topk_w   float32 [T, top_k] routing weights (used as given)
+ *   shared_w float32 [T, n_shared] or NULL (= 1.0)
+ *   y        bf16 [T, hidden] (output; fully overwritten)
+ *   workspace device buffer of >= mxm_workspace_bytes(l, T, top_k) bytes, exclusive to this call.
+ * One persistent launch runs all gate/up/down tiles of all experts (LPT-ordered task queue);
+ * route-prep, activation quantize+gather, planning and the top-k combine are separate short launches.
+ * Deterministic: identical inputs give bitwise identical y. */
+mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int32_t top_k, const int32_t* topk_ids,
+                              const float* topk_w, const float* shared_w, void* y, void* workspace, int64_t ws_bytes,
+                              mxm_stream stream);
+/* [sync] read (and clear) the device error word of the last call using `workspace`: *code = MXM_OK or MXM_E_DATA. */
+mxm_status mxm_poll_device_error(const mxm_layer* l, const void* workspace, mxm_stream stream, int32_t* code);
+/* Test/debug [sync]: number of tile tasks (gate/up, h-quant, down) the planner emitted in the last call
+ * on `workspace` (made with these T, top_k) and the number the persistent kernel executed (must be equal:
+ * every task runs exactly once). */
+mxm_status mxm_debug_task_stats(const mxm_layer* l, const void* workspace, int64_t T, int32_t top_k,
+                                mxm_stream stream, int32_t* n_tasks, int32_t* n_executed);
+
+/* Thread-local message for the last error returned on this thread. */
+const char* mxm_last_error(void);
+/* Library version string. */
+const char* mxm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MXMOE_H */

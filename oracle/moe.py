@@ -6,7 +6,7 @@ individually before aggregating the results". Expert e computes
 W_down^e( σ(W_gate^e X_e) ⊙ W_up^e X_e ) (Eq. 1) with σ = SiLU (reading R15)
 and the block output is F = Σ_e (...) ⊙ w_e (Eq. 2). Each linear block
 applies its own scheme (per-linear-block allocation): weight-only schemes
-multiply by the exactly dequantized weights; weight-activation schemes quantize the
+multiply by the dequantized weights rounded once to bf16 (R5); weight-activation schemes quantize the
 block input dynamically and accumulate exact integer products per group.
 Intermediate h is rounded to bf16 (reading R16).
 """
@@ -80,6 +80,15 @@ def quantize_block(w_bits_u16: np.ndarray, sch) -> QBlock:
     return QBlock(sch.w_bits, sch.a_bits, sch.w_group, sch.a_group, sch.symmetric, codes, s, z)
 
 
+def dequantize_weight_bf16(blk: "QBlock") -> np.ndarray:
+    """Weight-only dequantized operand: ŵ = bf16_rne(q·s + z), the exact value rounded once (reading R5).
+
+    The north star fixes parity "on identical dequantized weights"; a bf16 tensor-core path
+    multiplies bf16 operands, so the dequantized weight of a weight-only block is this bf16 value.
+    """
+    return bf16_round_f64(dequantize_weight(blk.codes, blk.scale, blk.zero, blk.w_group))
+
+
 def wa_int_accumulators(qa: np.ndarray, qw: np.ndarray, group: int) -> np.ndarray:
     """acc[g, m, n] = Σ_{k ∈ group g} qa[m,k]·qw[n,k], exact integers (reading G).
 
@@ -99,8 +108,8 @@ def linear_block(xin: np.ndarray, blk: QBlock) -> np.ndarray:
     xin = np.asarray(xin, dtype=np.float64)
     if blk.w_bits == 16:
         return xin @ bits_to_f64(blk.codes).T
-    if blk.a_bits == 16:  # weight-only: exact dequantized weights (R5)
-        return xin @ dequantize_weight(blk.codes, blk.scale, blk.zero, blk.w_group).T
+    if blk.a_bits == 16:  # weight-only: dequantized weights rounded once to bf16 (reading R5)
+        return xin @ dequantize_weight_bf16(blk).T
     qa, sa, _ = quantize_act(xin.astype(np.float32), blk.a_bits, blk.a_group)
     acc = wa_int_accumulators(qa, blk.codes, blk.w_group)
     y = np.zeros((xin.shape[0], blk.N))

@@ -1,0 +1,213 @@
+"""B200-native MxMoE mixed-precision MoE group-GEMM — thin torch binding over libmxmoe.so.
+
+Every function marshals torch CUDA tensors into the C ABI of include/mxmoe.h and runs on
+torch's current stream. All computation happens in the CUDA kernels of csrc/; nothing here
+computes (there is no CPU or eager fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import MxmError, check, load  # noqa: F401
+
+__all__ = ["Scheme", "quantize", "pack", "quantize_pack", "dequantize", "act_quant", "route_prep", "MoELayer",
+           "storage_bits_per_weight", "quant_sizes", "MxmError"]
+
+
+@dataclass(frozen=True)
+class Scheme:
+    """`wxay_gz_{sym,asym}`: a_bits 16 = weight-only; w_bits 16 = bf16."""
+
+    w_bits: int
+    a_bits: int = 16
+    w_group: int = -1
+    a_group: int = -1
+    symmetric: bool = False
+
+    def c(self) -> _lib.mxm_scheme:
+        return _lib.mxm_scheme(self.w_bits, self.a_bits, self.w_group, self.a_group, 1 if self.symmetric else 0)
+
+    @staticmethod
+    def of(s) -> "Scheme":
+        return s if isinstance(s, Scheme) else Scheme(s.w_bits, s.a_bits, s.w_group, s.a_group, bool(s.symmetric))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def quant_sizes(scheme, N: int, K: int) -> Tuple[int, int, int, int]:
+    s = Scheme.of(scheme).c()
+    cb, sb, zb, pb = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    check(load().mxm_quant_sizes(C.byref(s), N, K, C.byref(cb), C.byref(sb), C.byref(zb), C.byref(pb)))
+    return cb.value, sb.value, zb.value, pb.value
+
+
+def storage_bits_per_weight(scheme, K: int) -> float:
+    s = Scheme.of(scheme).c()
+    return load().mxm_storage_bits_per_weight(C.byref(s), K)
+
+
+def quantize(scheme, w: torch.Tensor, err: Optional[torch.Tensor] = None):
+    """W[N,K] bf16 (cuda) -> (codes uint8/int8 [N,K], scale bf16 [N,K/g], zero bf16 [N,K/g] or None)."""
+    sch = Scheme.of(scheme)
+    N, K = w.shape
+    assert w.dtype == torch.bfloat16 and w.is_cuda and w.is_contiguous()
+    g = K if sch.w_group == -1 else sch.w_group
+    codes = torch.empty(N, K, dtype=torch.int8 if sch.symmetric or sch.a_bits != 16 else torch.uint8, device=w.device)
+    scale = torch.empty(N, K // g, dtype=torch.bfloat16, device=w.device)
+    zero = None if (sch.symmetric or sch.a_bits != 16) else torch.empty(N, K // g, dtype=torch.bfloat16,
+                                                                           device=w.device)
+    s = sch.c()
+    check(load().mxm_quantize(C.byref(s), _ptr(w), N, K, _ptr(codes), _ptr(scale), _ptr(zero), _ptr(err), _stream()))
+    return codes, scale, zero
+
+
+def pack(scheme, codes: torch.Tensor, scale, zero, N: int, K: int) -> torch.Tensor:
+    sch = Scheme.of(scheme)
+    _, _, _, pb = quant_sizes(sch, N, K)
+    out = torch.empty(pb, dtype=torch.uint8, device=codes.device)
+    s = sch.c()
+    check(load().mxm_pack(C.byref(s), _ptr(codes), _ptr(scale), _ptr(zero), N, K, _ptr(out), _stream()))
+    return out
+
+
+def quantize_pack(scheme, w: torch.Tensor) -> torch.Tensor:
+    sch = Scheme.of(scheme)
+    N, K = w.shape
+    if sch.w_bits == 16:
+        return pack(sch, w.contiguous(), None, None, N, K)
+    codes, scale, zero = quantize(sch, w)
+    return pack(sch, codes, scale, zero, N, K)
+
+
+def dequantize(scheme, packed: torch.Tensor, N: int, K: int) -> torch.Tensor:
+    out = torch.empty(N, K, dtype=torch.float32, device=packed.device)
+    s = Scheme.of(scheme).c()
+    check(load().mxm_dequantize(C.byref(s), _ptr(packed), N, K, _ptr(out), _stream()))
+    return out
+
+
+def act_quant(v: torch.Tensor, a_bits: int, a_group: int = -1):
+    """Dynamic activation quantizer on v[M,K] bf16 -> (codes int8, scale f32 [M,K/g], qsum int32)."""
+    M, K = v.shape
+    g = K if a_group == -1 else a_group
+    codes = torch.empty(M, K, dtype=torch.int8, device=v.device)
+    scale = torch.empty(M, K // g, dtype=torch.float32, device=v.device)
+    qsum = torch.empty(M, K // g, dtype=torch.int32, device=v.device)
+    check(load().mxm_act_quant(_ptr(v), M, K, a_bits, a_group, _ptr(codes), _ptr(scale), _ptr(qsum), _stream()))
+    return codes, scale, qsum
+
+
+def route_prep(topk_ids: torch.Tensor, E: int):
+    """Step S1 on its own: (counts int32[E], offsets int32[E+1], perm int32[T*k], err int32[1])."""
+    T, k = topk_ids.shape
+    dev = topk_ids.device
+    counts = torch.zeros(E, dtype=torch.int32, device=dev)
+    offsets = torch.zeros(E + 1, dtype=torch.int32, device=dev)
+    perm = torch.full((T * k,), -1, dtype=torch.int32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    nch = (T * k + 2047) // 2048
+    scratch = torch.empty(max(256, nch * E * 4 + 256), dtype=torch.uint8, device=dev)
+    check(load().mxm_route_prep(_ptr(topk_ids.contiguous()), T, k, E, _ptr(counts), _ptr(offsets), _ptr(perm),
+                                _ptr(err), _ptr(scratch), scratch.numel(), _stream()))
+    return counts, offsets, perm, err
+
+
+class MoELayer:
+    """A quantized MoE layer: the per-(expert, block) precision table + packed weights on the GPU.
+
+    blocks: list over experts (routed then shared) of 3 (scheme, packed uint8 tensor) pairs
+    (gate, up, down), packed with `quantize_pack`.
+    """
+
+    def __init__(self, n_routed: int, n_shared: int, hidden: int, inter: int, shared_inter: int,
+                 blocks: Sequence[Sequence[Tuple[Scheme, torch.Tensor]]], device="cuda"):
+        lib = load()
+        self.n_routed, self.n_shared, self.hidden, self.inter, self.shared_inter = (n_routed, n_shared, hidden, inter,
+                                                                                     shared_inter)
+        V = n_routed + n_shared
+        assert len(blocks) == V and all(len(b) == 3 for b in blocks)
+        self._packed = [p for b in blocks for (_, p) in b]  # keep alive
+        self.schemes = [[Scheme.of(s) for (s, _) in b] for b in blocks]
+        arr = (_lib.mxm_linear * (3 * V))()
+        for v in range(V):
+            for j in range(3):
+                s, p = blocks[v][j]
+                arr[3 * v + j].scheme = Scheme.of(s).c()
+                arr[3 * v + j].packed = p.data_ptr()
+        self._desc = _lib.mxm_layer_desc(n_routed, n_shared, hidden, inter, shared_inter, arr)
+        self._arr = arr
+        nb = C.c_int64()
+        check(lib.mxm_layer_desc_bytes(C.byref(self._desc), C.byref(nb)))
+        self._desc_dev = torch.empty(nb.value, dtype=torch.uint8, device=device)
+        h = C.c_void_p()
+        check(lib.mxm_layer_init(C.byref(self._desc), _ptr(self._desc_dev), nb.value, None, C.byref(h)))
+        self._h = h
+        self._ws = None
+
+    @classmethod
+    def from_weights(cls, n_routed: int, n_shared: int, hidden: int, inter: int, shared_inter: int,
+                     weights: Sequence[Sequence[torch.Tensor]], table: Sequence[Sequence[Scheme]]) -> "MoELayer":
+        """Quantize + pack every (expert, block) on the GPU (mxm_quantize / mxm_pack) and build the layer.
+
+        weights[v] = (W_gate [f, d], W_up [f, d], W_down [d, f]) bf16 CUDA tensors; table[v] = 3 schemes.
+        """
+        blocks = []
+        for v in range(n_routed + n_shared):
+            blocks.append([(Scheme.of(table[v][j]), quantize_pack(table[v][j], weights[v][j].contiguous()))
+                           for j in range(3)])
+        return cls(n_routed, n_shared, hidden, inter, shared_inter, blocks, device=weights[0][0].device)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                load().mxm_layer_free(self._h)
+        except Exception:
+            pass
+
+    def workspace_bytes(self, T: int, top_k: int) -> int:
+        nb = C.c_int64()
+        check(load().mxm_workspace_bytes(self._h, T, top_k, C.byref(nb)))
+        return nb.value
+
+    def workspace(self, T: int, top_k: int) -> torch.Tensor:
+        nb = self.workspace_bytes(T, top_k)
+        if self._ws is None or self._ws.numel() < nb:
+            self._ws = torch.empty(nb, dtype=torch.uint8, device=self._desc_dev.device)
+        return self._ws
+
+    def __call__(self, x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor,
+                 shared_w: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                 workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+        T = x.shape[0]
+        k = topk_ids.shape[1]
+        assert x.dtype == torch.bfloat16 and x.is_contiguous() and topk_ids.dtype == torch.int32
+        assert topk_w.dtype == torch.float32
+        if out is None:
+            out = torch.empty(T, self.hidden, dtype=torch.bfloat16, device=x.device)
+        ws = workspace if workspace is not None else self.workspace(T, k)
+        check(load().mxm_moe_group_gemm(self._h, _ptr(x), T, k, _ptr(topk_ids), _ptr(topk_w), _ptr(shared_w),
+                                        _ptr(out), _ptr(ws), ws.numel(), _stream()))
+        return out
+
+    def poll_error(self, workspace: Optional[torch.Tensor] = None) -> int:
+        code = C.c_int32()
+        ws = workspace if workspace is not None else self._ws
+        check(load().mxm_poll_device_error(self._h, _ptr(ws), _stream(), C.byref(code)))
+        return code.value
+
+    def task_stats(self, T: int, top_k: int, workspace: Optional[torch.Tensor] = None) -> Tuple[int, int]:
+        a, b = C.c_int32(), C.c_int32()
+        ws = workspace if workspace is not None else self._ws
+        check(load().mxm_debug_task_stats(self._h, _ptr(ws), T, top_k, _stream(), C.byref(a), C.byref(b)))
+        return a.value, b.value

@@ -1,0 +1,397 @@
+// api.cu — the C ABI (include/mxmoe.h): host-side validation, layer descriptor table, workspace
+// carving, TMA tensor maps and the launch sequence of the hot path (S1 route-prep -> S2 act-quant
+// + gather -> S3 plan -> S4-S7 persistent group-GEMM -> S8 combine), all on the caller's stream.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mxmoe.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace mxm;
+
+namespace {
+thread_local std::string g_err;
+
+mxm_status fail(mxm_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+mxm_status cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return MXM_E_CUDA;
+}
+#define MXM_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool encode_2d(CUtensorMap* m, const void* base, bool bf16, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const uint32_t esz = bf16 ? 2 : 1;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * esz};
+  cuuint32_t box[2] = {128u / esz, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = kNumSms;
+  }
+  return n;
+}
+
+int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
+}  // namespace
+
+struct mxm_layer {
+  int E, S, V, d, f, fs, f_max;
+  std::vector<ExpertDesc> ex;
+  ExpertDesc* ex_dev;
+  bool need_xb, need_xqa, need_xqb, need_hq;
+};
+
+// workspace layout for T tokens, k routes
+struct WsLayout {
+  int64_t R, g_max, task_cap;
+  int64_t err, route_scratch, counts, v_off, row_src, row_w, row_exp, inv;
+  int64_t Xb, XqA, XsA, XqB, XsB, H, Hq, Hs, O;
+  int64_t tasks, meta, grp_n1, grp_nq, p1_done, hq_done;
+  int64_t total;
+};
+
+static WsLayout make_layout(const mxm_layer* l, int64_t T, int k) {
+  WsLayout w{};
+  const int64_t R = T * k + T * l->S;
+  w.R = R;
+  w.g_max = (R + 15) / 16 + l->V + 1;
+  w.task_cap = w.g_max * (l->f_max / 128 + 4 + l->d / 128);
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    int64_t at = o;
+    o += align256(bytes > 0 ? bytes : 1);
+    return at;
+  };
+  w.err = take(256);
+  w.route_scratch = take(route_scratch_bytes(T * k, l->E));
+  w.counts = take(4 * (l->E + 1));
+  w.v_off = take(4 * (l->V + 1));
+  w.row_src = take(4 * R);
+  w.row_w = take(4 * R);
+  w.row_exp = take(4 * R);
+  w.inv = take(4 * T * k);
+  w.Xb = l->need_xb ? take(2 * R * l->d) : -1;
+  w.XqA = l->need_xqa ? take(R * l->d) : -1;
+  w.XsA = l->need_xqa ? take(4 * R * (l->d / 128)) : -1;
+  w.XqB = l->need_xqb ? take(R * l->d) : -1;
+  w.XsB = l->need_xqb ? take(4 * R * (l->d / 128)) : -1;
+  w.H = take(2 * R * l->f_max);
+  w.Hq = l->need_hq ? take(R * l->f_max) : -1;
+  w.Hs = l->need_hq ? take(4 * R * (l->f_max / 128)) : -1;
+  w.O = take(2 * R * l->d);
+  w.tasks = take(16 * w.task_cap);
+  w.meta = take(4 * (8 + 4 * w.g_max));
+  w.grp_n1 = take(4 * w.g_max);
+  w.grp_nq = take(4 * w.g_max);
+  w.p1_done = take(4 * w.g_max);
+  w.hq_done = take(4 * w.g_max);
+  w.total = o;
+  return w;
+}
+
+extern "C" {
+
+const char* mxm_last_error(void) { return g_err.c_str(); }
+const char* mxm_version(void) { return "mxmoe-b200 0.1 (sm_100a)"; }
+
+mxm_status mxm_scheme_check(const mxm_scheme* s, int64_t N, int64_t K) {
+  if (!s) return fail(MXM_E_CONFIG, "null scheme");
+  PackGeom g;
+  if (make_geom(*s, N, K, &g) != MXM_OK) return fail(MXM_E_CONFIG, "unsupported scheme/shape");
+  return MXM_OK;
+}
+
+mxm_status mxm_quant_sizes(const mxm_scheme* s, int64_t N, int64_t K, int64_t* codes_bytes, int64_t* scale_bytes,
+                           int64_t* zero_bytes, int64_t* packed_bytes) {
+  if (!s) return fail(MXM_E_CONFIG, "null scheme");
+  PackGeom g;
+  if (make_geom(*s, N, K, &g) != MXM_OK) return fail(MXM_E_CONFIG, "unsupported scheme/shape");
+  const int64_t ng = K / g.group;
+  if (codes_bytes) *codes_bytes = s->w_bits == 16 ? N * K * 2 : N * K;
+  if (scale_bytes) *scale_bytes = s->w_bits == 16 ? 0 : N * ng * 2;
+  if (zero_bytes) *zero_bytes = (s->w_bits == 16 || g.sym) ? 0 : N * ng * 2;
+  if (packed_bytes) *packed_bytes = g.total_bytes;
+  return MXM_OK;
+}
+
+double mxm_storage_bits_per_weight(const mxm_scheme* s, int64_t K) {
+  if (!s) return 0.0;
+  if (s->w_bits == 16) return 16.0;
+  const double g = s->w_group == -1 ? (double)K : (double)s->w_group;
+  const bool sym = s->symmetric || s->a_bits != 16;
+  return s->w_bits + (sym ? 1.0 : 2.0) * 16.0 / g;
+}
+
+mxm_status mxm_quantize(const mxm_scheme* s, const void* w, int64_t N, int64_t K, void* codes, void* scale, void* zero,
+                        int32_t* err, mxm_stream stream) {
+  if (!s || !w || !codes || !scale) return fail(MXM_E_CONFIG, "null argument");
+  if (s->w_bits == 16) return fail(MXM_E_CONFIG, "w16 has nothing to quantize");
+  PackGeom g;
+  if (make_geom(*s, N, K, &g) != MXM_OK) return fail(MXM_E_CONFIG, "unsupported scheme/shape");
+  if (!g.sym && !zero) return fail(MXM_E_CONFIG, "asymmetric scheme needs a zero buffer");
+  MXM_CUDA(launch_quantize(g, w, codes, scale, zero, err, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_pack(const mxm_scheme* s, const void* codes, const void* scale, const void* zero, int64_t N, int64_t K,
+                    void* packed, mxm_stream stream) {
+  if (!s || !codes || !packed) return fail(MXM_E_CONFIG, "null argument");
+  PackGeom g;
+  if (make_geom(*s, N, K, &g) != MXM_OK) return fail(MXM_E_CONFIG, "unsupported scheme/shape");
+  if (s->w_bits != 16 && !scale) return fail(MXM_E_CONFIG, "null scale");
+  if (g.kind == KIND_WO && !g.sym && !zero) return fail(MXM_E_CONFIG, "null zero");
+  MXM_CUDA(launch_pack(g, codes, scale, zero, packed, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_dequantize(const mxm_scheme* s, const void* packed, int64_t N, int64_t K, float* out,
+                          mxm_stream stream) {
+  if (!s || !packed || !out) return fail(MXM_E_CONFIG, "null argument");
+  PackGeom g;
+  if (make_geom(*s, N, K, &g) != MXM_OK) return fail(MXM_E_CONFIG, "unsupported scheme/shape");
+  MXM_CUDA(launch_dequantize(g, packed, out, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_act_quant(const void* v, int64_t M, int64_t K, int32_t a_bits, int32_t a_group, void* codes,
+                         float* scale, int32_t* qsum, mxm_stream stream) {
+  if (!v || !codes || !scale) return fail(MXM_E_CONFIG, "null argument");
+  if (!(a_bits == 4 || a_bits == 5 || a_bits == 8)) return fail(MXM_E_CONFIG, "a_bits must be 4, 5 or 8");
+  const int64_t g = a_group == -1 ? K : a_group;
+  if (M < 0 || K <= 0 || K % 128 != 0 || !(a_group == -1 || a_group == 128)) return fail(MXM_E_CONFIG, "bad shape");
+  if (M == 0) return MXM_OK;
+  MXM_CUDA(launch_act_quant(v, M, K, a_bits, (int)g, codes, scale, qsum, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_route_prep(const int32_t* topk_ids, int64_t T, int32_t k, int32_t E, int32_t* counts, int32_t* offsets,
+                          int32_t* perm, int32_t* err, void* scratch, int64_t scratch_bytes, mxm_stream stream) {
+  if (!topk_ids || !counts || !offsets || !perm) return fail(MXM_E_CONFIG, "null argument");
+  if (E <= 0 || E > 256 || k <= 0 || k > 32 || T < 0) return fail(MXM_E_CONFIG, "bad E/k/T");
+  if (scratch_bytes < route_scratch_bytes(T * k, E)) return fail(MXM_E_CONFIG, "scratch too small");
+  MXM_CUDA(launch_route_prep(topk_ids, nullptr, T, k, E, 0, nullptr, counts, offsets, nullptr, perm, nullptr, nullptr,
+                             nullptr, nullptr, err, scratch, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_layer_desc_bytes(const mxm_layer_desc* d, int64_t* bytes) {
+  if (!d || !bytes) return fail(MXM_E_CONFIG, "null argument");
+  *bytes = (int64_t)sizeof(ExpertDesc) * (d->n_routed + d->n_shared);
+  return MXM_OK;
+}
+
+mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_bytes, const void* tile_costs,
+                          mxm_layer** out) {
+  (void)tile_costs;
+  if (!d || !d->blocks || !desc_dev || !out) return fail(MXM_E_CONFIG, "null argument");
+  const int E = d->n_routed, S = d->n_shared, V = E + S;
+  if (E <= 0 || E > 256 || S < 0 || V > 256) return fail(MXM_E_CONFIG, "expert count out of range");
+  if (d->hidden <= 0 || d->hidden % 128 || d->inter <= 0 || d->inter % 128) return fail(MXM_E_CONFIG, "hidden/inter % 128");
+  if (S > 0 && (d->shared_inter <= 0 || d->shared_inter % 128)) return fail(MXM_E_CONFIG, "shared_inter % 128");
+  if (desc_bytes < (int64_t)sizeof(ExpertDesc) * V) return fail(MXM_E_CONFIG, "descriptor buffer too small");
+  auto* l = new mxm_layer();
+  l->E = E;
+  l->S = S;
+  l->V = V;
+  l->d = d->hidden;
+  l->f = d->inter;
+  l->fs = S > 0 ? d->shared_inter : 0;
+  l->f_max = l->f > l->fs ? l->f : l->fs;
+  l->need_xb = l->need_xqa = l->need_xqb = l->need_hq = false;
+  l->ex.resize(V);
+  for (int v = 0; v < V; ++v) {
+    ExpertDesc& e = l->ex[v];
+    memset(&e, 0, sizeof(e));
+    const int f = v < E ? l->f : l->fs;
+    e.inter = f;
+    e.shared = v >= E;
+    for (int j = 0; j < 3; ++j) {
+      const mxm_linear& b = d->blocks[v * 3 + j];
+      const int64_t N = j < 2 ? f : l->d, K = j < 2 ? l->d : f;
+      if (!b.packed) {
+        delete l;
+        return fail(MXM_E_CONFIG, "null packed block");
+      }
+      PackGeom g;
+      if (make_geom(b.scheme, N, K, &g) != MXM_OK) {
+        delete l;
+        char buf[160];
+        snprintf(buf, sizeof buf, "expert %d block %d: unsupported scheme w%d a%d g%d for [%lld, %lld]", v, j,
+                 b.scheme.w_bits, b.scheme.a_bits, b.scheme.w_group, (long long)N, (long long)K);
+        return fail(MXM_E_CONFIG, buf);
+      }
+      e.blk[j].packed = reinterpret_cast<const uint8_t*>(b.packed);
+      e.blk[j].geo = g;
+      e.blk[j].a_bits = b.scheme.a_bits;
+      e.blk[j].a_group = b.scheme.a_bits == 16 ? -1 : b.scheme.a_group;
+    }
+    const mxm_scheme& sg = d->blocks[v * 3 + 0].scheme;
+    const mxm_scheme& su = d->blocks[v * 3 + 1].scheme;
+    e.same_gu = sg.w_bits == su.w_bits && sg.a_bits == su.a_bits && sg.w_group == su.w_group &&
+                (sg.a_bits == 16 ? 1 : sg.a_group == su.a_group) && (sg.symmetric != 0) == (su.symmetric != 0);
+    // input slots
+    const bool gwa = sg.a_bits != 16, uwa = su.a_bits != 16;
+    e.blk[0].in_slot = gwa ? 1 : 0;
+    if (!uwa)
+      e.blk[1].in_slot = 0;
+    else if (gwa && sg.a_bits == su.a_bits && e.blk[0].a_group == e.blk[1].a_group)
+      e.blk[1].in_slot = 1;
+    else
+      e.blk[1].in_slot = gwa ? 2 : 1;
+    e.blk[2].in_slot = d->blocks[v * 3 + 2].scheme.a_bits != 16 ? 1 : 0;
+    for (int j = 0; j < 2; ++j) {
+      if (e.blk[j].in_slot == 0) l->need_xb = true;
+      if (e.blk[j].in_slot == 1) l->need_xqa = true;
+      if (e.blk[j].in_slot == 2) l->need_xqb = true;
+    }
+    if (e.blk[2].in_slot == 1) l->need_hq = true;
+  }
+  cudaError_t ce = cudaMemcpy(desc_dev, l->ex.data(), sizeof(ExpertDesc) * V, cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) {
+    delete l;
+    return cuda_fail(ce, "cudaMemcpy(desc)");
+  }
+  l->ex_dev = reinterpret_cast<ExpertDesc*>(desc_dev);
+  *out = l;
+  return MXM_OK;
+}
+
+void mxm_layer_free(mxm_layer* l) { delete l; }
+
+mxm_status mxm_workspace_bytes(const mxm_layer* l, int64_t max_tokens, int32_t top_k, int64_t* bytes) {
+  if (!l || !bytes || max_tokens < 0 || top_k <= 0 || top_k > 32) return fail(MXM_E_CONFIG, "bad argument");
+  *bytes = make_layout(l, max_tokens, top_k).total;
+  return MXM_OK;
+}
+
+mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int32_t k, const int32_t* topk_ids,
+                              const float* topk_w, const float* shared_w, void* y, void* ws, int64_t ws_bytes,
+                              mxm_stream stream) {
+  if (!l || !ws || (T > 0 && (!x || !topk_ids || !topk_w || !y))) return fail(MXM_E_CONFIG, "null argument");
+  if (k <= 0 || k > 32 || T < 0) return fail(MXM_E_CONFIG, "bad top_k / T");
+  const WsLayout w = make_layout(l, T, k);
+  if (ws_bytes < w.total) return fail(MXM_E_CONFIG, "workspace too small");
+  if (w.R >= (1LL << 31) || w.task_cap >= (1LL << 31)) return fail(MXM_E_CONFIG, "too many tokens");
+  if (T == 0) return MXM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* b = reinterpret_cast<uint8_t*>(ws);
+  auto P = [&](int64_t off) -> void* { return off < 0 ? nullptr : (void*)(b + off); };
+  int32_t* err = (int32_t*)P(w.err);
+  int32_t* v_off = (int32_t*)P(w.v_off);
+  int32_t* row_src = (int32_t*)P(w.row_src);
+  float* row_w = (float*)P(w.row_w);
+  int32_t* row_exp = (int32_t*)P(w.row_exp);
+  int32_t* inv = (int32_t*)P(w.inv);
+
+  MXM_CUDA(cudaMemsetAsync(err, 0, 4, st));
+  // S1 route prep
+  MXM_CUDA(launch_route_prep(topk_ids, topk_w, T, k, l->E, l->S, shared_w, (int32_t*)P(w.counts), nullptr, v_off,
+                             nullptr, row_src, row_w, row_exp, inv, err, P(w.route_scratch), st));
+  // S2 activation quantize + gather
+  MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
+                               (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), st));
+  // S3 plan
+  MXM_CUDA(launch_plan(l->ex_dev, l->V, l->E, T, l->d, v_off, (int)w.g_max, w.task_cap, (Task*)P(w.tasks),
+                       (int32_t*)P(w.meta), (int32_t*)P(w.grp_n1), (int32_t*)P(w.grp_nq), (int32_t*)P(w.p1_done),
+                       (int32_t*)P(w.hq_done), st));
+  // S4-S7 persistent group GEMM
+  GemmParams prm;
+  memset(&prm, 0, sizeof(prm));
+  const uint32_t boxes[4] = {16, 32, 64, 128};
+  const void* srcs[5] = {P(w.Xb), P(w.XqA), P(w.XqB), P(w.H), P(w.Hq)};
+  const bool isbf[5] = {true, false, false, true, false};
+  const uint64_t cols[5] = {(uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->f_max, (uint64_t)l->f_max};
+  for (int i = 0; i < 5; ++i) {
+    if (!srcs[i]) continue;
+    for (int j = 0; j < 4; ++j)
+      if (!encode_2d(&prm.tmap[i][j], srcs[i], isbf[i], cols[i], (uint64_t)w.R, boxes[j]))
+        return fail(MXM_E_CUDA, "cuTensorMapEncodeTiled failed");
+  }
+  prm.ex = l->ex_dev;
+  prm.tasks = (const Task*)P(w.tasks);
+  prm.meta = (int32_t*)P(w.meta);
+  prm.p1_done = (int32_t*)P(w.p1_done);
+  prm.hq_done = (int32_t*)P(w.hq_done);
+  prm.grp_n1 = (const int32_t*)P(w.grp_n1);
+  prm.grp_nq = (const int32_t*)P(w.grp_nq);
+  prm.xs[0] = nullptr;
+  prm.xs[1] = (const float*)P(w.XsA);
+  prm.xs[2] = (const float*)P(w.XsB);
+  prm.H = (uint16_t*)P(w.H);
+  prm.Hq = (int8_t*)P(w.Hq);
+  prm.Hs = (float*)P(w.Hs);
+  prm.O = (uint16_t*)P(w.O);
+  prm.row_w = row_w;
+  prm.d = l->d;
+  prm.f_max = l->f_max;
+  MXM_CUDA(launch_moe_gemm(prm, num_sms(), st));
+  // S8 combine
+  MXM_CUDA(launch_combine(P(w.O), l->d, T, k, l->S, inv, y, st));
+  return MXM_OK;
+}
+
+mxm_status mxm_poll_device_error(const mxm_layer* l, const void* ws, mxm_stream stream, int32_t* code) {
+  if (!l || !ws || !code) return fail(MXM_E_CONFIG, "null argument");
+  int32_t v = 0;
+  MXM_CUDA(cudaMemcpyAsync(&v, ws, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  MXM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  MXM_CUDA(cudaMemsetAsync(const_cast<void*>(ws), 0, 4, (cudaStream_t)stream));
+  *code = v ? MXM_E_DATA : MXM_OK;
+  return MXM_OK;
+}
+
+mxm_status mxm_debug_task_stats(const mxm_layer* l, const void* ws, int64_t T, int32_t top_k, mxm_stream stream,
+                                int32_t* n_tasks, int32_t* n_executed) {
+  if (!l || !ws || !n_tasks || !n_executed || top_k <= 0) return fail(MXM_E_CONFIG, "null argument");
+  const WsLayout w = make_layout(l, T, top_k);
+  int32_t meta[8];
+  MXM_CUDA(cudaMemcpyAsync(meta, (const uint8_t*)ws + w.meta, sizeof(meta), cudaMemcpyDeviceToHost,
+                           (cudaStream_t)stream));
+  MXM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  *n_tasks = meta[0];
+  *n_executed = meta[6];
+  return MXM_OK;
+}
+
+}  // extern "C"

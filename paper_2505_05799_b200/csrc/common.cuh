@@ -1,0 +1,119 @@
+// common.cuh — structures shared by the host runtime and the device kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/mxmoe.h"
+
+namespace mxm {
+
+constexpr int kNumSms = 148;
+constexpr int kRowsPerTile = 128;  // output channels per tile (UMMA M)
+
+// Packed-format kinds (docs/packed_format.md)
+enum Kind : int8_t {
+  KIND_W16 = 0,     // F16 image chunks (bf16 pass-through)
+  KIND_WO = 1,      // F16 row-word chunks, weight-only w2/w3/w4/w8 -> dequant to bf16
+  KIND_WA_ROW = 2,  // I8 row-word chunks, w4a4 / w5a5 -> unpack to s8
+  KIND_WA_IMG = 3,  // I8 image chunks, w8a8
+};
+
+__host__ __device__ inline bool kind_is_i8(int k) { return k >= KIND_WA_ROW; }
+__host__ __device__ inline bool kind_needs_transform(int k) { return k == KIND_WO || k == KIND_WA_ROW; }
+
+// Geometry of one packed linear block W[N, K].
+struct PackGeom {
+  int32_t N, K;
+  int8_t kind, w_bits, a_bits, sym;
+  int32_t group;        // effective group (K for per-channel)
+  int32_t ks;           // stage elements (64 F16, 128 I8)
+  int32_t ns;           // stages = K / ks
+  int32_t code_bytes;   // code bytes per chunk
+  int32_t meta_bytes;   // meta bytes at a group-start chunk (WO only)
+  int64_t rb_bytes;     // bytes per 128-row block
+  int64_t wa_scale_off; // byte offset of the I8 weight-scale array [K/g][N]
+  int64_t total_bytes;
+};
+
+__host__ __device__ inline int64_t chunk_offset(const PackGeom& g, int rb, int ks) {
+  const int64_t starts = ((int64_t)ks * g.ks + g.group - 1) / g.group;  // group starts before stage ks
+  return (int64_t)rb * g.rb_bytes + (int64_t)ks * g.code_bytes + (g.kind == KIND_WO ? starts * g.meta_bytes : 0);
+}
+__host__ __device__ inline bool chunk_has_meta(const PackGeom& g, int ks) {
+  return g.kind == KIND_WO && ((int64_t)ks * g.ks) % g.group == 0;
+}
+
+// Device descriptor of one linear block inside a layer.
+struct LinDesc {
+  const uint8_t* packed;
+  PackGeom geo;
+  int32_t in_slot;   // gate/up: 0 = bf16 X, 1 = i8 slot A, 2 = i8 slot B; down: 0 = bf16 H, 1 = i8 H
+  int32_t a_bits, a_group;
+};
+
+// One (virtual) expert: routed experts 0..E-1, then shared experts.
+struct ExpertDesc {
+  LinDesc blk[3];
+  int32_t inter;      // f of this expert
+  int32_t same_gu;    // gate and up share the scheme (one sub-loop, shared B tile)
+  int32_t shared;     // 1 = shared expert (all tokens)
+  int32_t pad;
+};
+
+// Task descriptor (16 bytes), produced by the plan kernel, consumed by the persistent kernel.
+struct Task {
+  uint16_t expert;
+  uint8_t phase;   // 0 gate/up, 1 h-quant, 2 down, 255 stop
+  uint8_t nt;      // token tile (16/32/64/128); h-quant: sub-chunk index
+  int32_t row0;    // first route row of the m-tile (group)
+  uint16_t rows;   // valid rows in the m-tile
+  uint16_t ntile;  // 128-channel output tile index (h-quant: unused)
+  int32_t gid;     // m-tile group id (dependency counters)
+};
+static_assert(sizeof(Task) == 16, "task size");
+
+}  // namespace mxm
+
+namespace mxm {
+// Validate a scheme for W[N, K] and fill its packed geometry. Returns MXM_OK or MXM_E_CONFIG.
+__host__ __device__ inline mxm_status make_geom(const mxm_scheme& s, int64_t N, int64_t K, PackGeom* g) {
+  if (N <= 0 || K <= 0 || N % 128 != 0 || N > (1 << 24) || K > (1 << 24)) return MXM_E_CONFIG;
+  PackGeom r{};
+  r.N = (int32_t)N;
+  r.K = (int32_t)K;
+  r.w_bits = (int8_t)s.w_bits;
+  r.a_bits = (int8_t)s.a_bits;
+  r.sym = (int8_t)(s.symmetric ? 1 : 0);
+  if (s.w_bits == 16) {
+    if (s.a_bits != 16) return MXM_E_CONFIG;
+    r.kind = KIND_W16;
+    r.ks = 64;
+    r.group = (int32_t)K;
+    r.sym = 1;
+  } else if (s.a_bits == 16) {
+    if (!(s.w_bits == 2 || s.w_bits == 3 || s.w_bits == 4 || s.w_bits == 8)) return MXM_E_CONFIG;
+    if (!(s.w_group == -1 || s.w_group == 64 || s.w_group == 128)) return MXM_E_CONFIG;
+    r.kind = KIND_WO;
+    r.ks = 64;
+    r.group = s.w_group == -1 ? (int32_t)K : s.w_group;
+  } else {
+    if (s.a_bits != s.w_bits || !s.symmetric) return MXM_E_CONFIG;
+    if (!(s.w_bits == 4 || s.w_bits == 5 || s.w_bits == 8)) return MXM_E_CONFIG;
+    if (!(s.w_group == -1 || s.w_group == 128) || s.a_group != s.w_group) return MXM_E_CONFIG;
+    r.kind = s.w_bits == 8 ? KIND_WA_IMG : KIND_WA_ROW;
+    r.ks = 128;
+    r.group = s.w_group == -1 ? (int32_t)K : s.w_group;
+  }
+  if (K % r.ks != 0 || K % r.group != 0) return MXM_E_CONFIG;
+  r.ns = (int32_t)(K / r.ks);
+  r.code_bytes = r.kind == KIND_W16 ? 16384 : 128 * r.ks * s.w_bits / 8;
+  r.meta_bytes = r.kind == KIND_WO ? (r.sym ? 256 : 512) : 0;
+  const int64_t ng = K / r.group;
+  r.rb_bytes = (int64_t)r.ns * r.code_bytes + (r.kind == KIND_WO ? ng * r.meta_bytes : 0);
+  r.wa_scale_off = (N / 128) * r.rb_bytes;
+  r.total_bytes = r.wa_scale_off + (kind_is_i8(r.kind) ? ng * N * 2 : 0);
+  *g = r;
+  return MXM_OK;
+}
+}  // namespace mxm

@@ -1,0 +1,52 @@
+// kernels.h — host-callable launchers of the device kernels (internal to libmxmoe).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace mxm {
+
+struct GemmParams {
+  CUtensorMap tmap[5][4];  // B sources {Xb, XqA, XqB, H, Hq} x token tile {16, 32, 64, 128}
+  const ExpertDesc* ex;
+  const Task* tasks;
+  int32_t* meta;  // [0] n_tasks, [5] queue head, [6] executed tasks
+  int32_t* p1_done;
+  int32_t* hq_done;
+  const int32_t* grp_n1;
+  const int32_t* grp_nq;
+  const float* xs[3];  // activation scales of the gate/up input slots (index 1, 2)
+  uint16_t* H;
+  int8_t* Hq;
+  float* Hs;
+  uint16_t* O;
+  const float* row_w;
+  int d, f_max;
+};
+
+cudaError_t launch_quantize(const PackGeom& g, const void* w, void* codes, void* scale, void* zero, int32_t* err,
+                            cudaStream_t st);
+cudaError_t launch_pack(const PackGeom& g, const void* codes, const void* scale, const void* zero, void* out,
+                        cudaStream_t st);
+cudaError_t launch_dequantize(const PackGeom& g, const void* packed, float* out, cudaStream_t st);
+cudaError_t launch_act_quant(const void* v, int64_t M, int64_t K, int a_bits, int group, void* codes, float* scale,
+                             int32_t* qsum, cudaStream_t st);
+
+int64_t route_scratch_bytes(int64_t n_routes, int E);
+cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T, int k, int E, int S,
+                              const float* shared_w, int32_t* counts, int32_t* offsets, int32_t* v_off, int32_t* perm,
+                              int32_t* row_src, float* row_w, int32_t* row_exp, int32_t* inv, int32_t* err,
+                              void* scratch, cudaStream_t st);
+cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, const int32_t* row_exp,
+                                const int32_t* v_off, int V, const ExpertDesc* ex, int64_t R, void* Xb, void* XqA,
+                                float* XsA, void* XqB, float* XsB, cudaStream_t st);
+cudaError_t launch_combine(const void* O, int d, int64_t T, int k, int S, const int32_t* inv, void* y,
+                           cudaStream_t st);
+cudaError_t launch_plan(const ExpertDesc* ex, int V, int E, int64_t T, int d, const int32_t* v_off, int g_max,
+                        int64_t task_cap, Task* tasks, int32_t* meta, int32_t* grp_n1, int32_t* grp_nq,
+                        int32_t* p1_done, int32_t* hq_done, cudaStream_t st);
+cudaError_t launch_moe_gemm(const GemmParams& prm, int grid, cudaStream_t st);
+
+}  // namespace mxm

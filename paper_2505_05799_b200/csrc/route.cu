@@ -1,0 +1,245 @@
+// route.cu — step S1 (route preparation) and S2 (activation quantize + gather) and S8 (combine).
+//
+// S1: histogram of the T*k expert ids, exclusive scan, stable (t, j)-ordered placement
+//     (the GPU form of "each expert is processed individually": rows of one expert are
+//     contiguous). Shared experts (always active) occupy rows [s*T, (s+1)*T) first; routed rows
+//     follow at S*T + offsets[e].
+// S2: per route row, the block inputs of its expert's gate/up: a bf16 copy (weight-only schemes)
+//     and/or int8 codes + fp32 scales of the dynamic activation quantizer.
+// S8: y[t] = sum_j O[row(t, j)] + sum_s O[s*T + t]  (Eq. 2; w_e already applied), fixed order.
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "actq.cuh"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mxm {
+
+constexpr int kRouteChunk = 2048;
+constexpr int kMaxExperts = 1024;
+
+// ---- S1a: per-chunk histograms; invalid ids -> error word
+__global__ void route_count_kernel(const int32_t* __restrict__ ids, int64_t n, int E, int32_t* __restrict__ chunk_hist,
+                                   int32_t* err) {
+  __shared__ int32_t hist[kMaxExperts];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRouteChunk;
+  for (int i = threadIdx.x; i < kRouteChunk; i += blockDim.x) {
+    const int64_t r = base + i;
+    if (r >= n) break;
+    const int e = ids[r];
+    if (e >= 0 && e < E)
+      atomicAdd(&hist[e], 1);
+    else if (e != -1 && err)
+      atomicExch(err, (int32_t)MXM_E_DATA);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) chunk_hist[(int64_t)blockIdx.x * E + e] = hist[e];
+}
+
+// ---- S1b: single block: chunk bases, counts, offsets, virtual-expert row offsets
+__global__ void route_scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E, int S, int64_t T,
+                                  int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
+                                  int32_t* __restrict__ v_off) {
+  __shared__ int32_t tot[kMaxExperts];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t run = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int32_t h = chunk_hist[(int64_t)c * E + e];
+      chunk_hist[(int64_t)c * E + e] = run;  // becomes the chunk's base within expert e
+      run += h;
+    }
+    tot[e] = run;
+    if (counts) counts[e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      if (offsets) offsets[e] = run;
+      if (v_off) v_off[e] = (int32_t)(S * T) + run;
+      run += tot[e];
+    }
+    if (offsets) offsets[E] = run;
+    if (v_off) {
+      v_off[E + S] = (int32_t)(S * T) + run;  // end of routed rows
+      for (int s = 0; s < S; ++s) v_off[E + s] = (int32_t)(s * T);
+    }
+  }
+}
+
+// ---- S1c: stable placement within chunk (warp match + per-warp counts)
+__global__ void route_place_kernel(const int32_t* __restrict__ ids, const float* __restrict__ topk_w, int64_t n, int k,
+                                   int E, int64_t row_base, const int32_t* __restrict__ chunk_base,
+                                   const int32_t* __restrict__ offsets_or_null, const int32_t* __restrict__ v_off,
+                                   int32_t* __restrict__ perm, int32_t* __restrict__ row_src,
+                                   float* __restrict__ row_w, int32_t* __restrict__ row_exp, int32_t* __restrict__ inv) {
+  __shared__ int32_t base[kMaxExperts];
+  __shared__ int32_t wcnt[8][kMaxExperts / 4];  // 8 warps; E <= 256 in this path
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    base[e] = chunk_base[(int64_t)blockIdx.x * E + e] + (offsets_or_null ? offsets_or_null[e] : v_off[e] - (int32_t)row_base);
+  const int64_t c0 = (int64_t)blockIdx.x * kRouteChunk;
+  for (int sub = 0; sub < kRouteChunk; sub += 256) {
+    for (int i = threadIdx.x; i < 8 * E; i += blockDim.x) wcnt[i / E][i % E] = 0;
+    __syncthreads();
+    const int64_t r = c0 + sub + threadIdx.x;
+    int e = -1;
+    if (r < n) e = ids[r];
+    if (e >= E || e < 0) e = -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(peers & ((1u << lane) - 1));
+    if (e >= 0 && rank == 0) wcnt[warp][e] = __popc(peers);
+    __syncthreads();
+    if (e >= 0) {
+      int pos = base[e] + rank;
+      for (int w = 0; w < warp; ++w) pos += wcnt[w][e];
+      if (perm) perm[pos] = (int32_t)r;
+      const int64_t row = row_base + pos;
+      if (row_src) {
+        row_src[row] = (int32_t)(r / k);
+        row_w[row] = topk_w[r];
+        row_exp[row] = e;
+        inv[r] = (int32_t)row;
+      }
+    } else if (r < n && inv) {
+      inv[r] = -1;
+    }
+    __syncthreads();
+    for (int ee = threadIdx.x; ee < E; ee += blockDim.x) {
+      int s = 0;
+      for (int w = 0; w < 8; ++w) s += wcnt[w][ee];
+      base[ee] += s;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- shared-expert rows
+__global__ void route_shared_kernel(int64_t T, int E, int S, const float* __restrict__ shared_w,
+                                    int32_t* __restrict__ row_src, float* __restrict__ row_w, int32_t* __restrict__ row_exp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= T * S) return;
+  const int64_t s = i / T, t = i % T;
+  row_src[i] = (int32_t)t;
+  row_w[i] = shared_w ? shared_w[t * S + s] : 1.0f;
+  row_exp[i] = E + (int32_t)s;
+}
+
+// ---- S2: one warp per route row: gather / quantize the gate/up inputs of the row's expert
+__global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const int32_t* __restrict__ row_src,
+                                    const int32_t* __restrict__ row_exp, const int32_t* __restrict__ v_off, int V,
+                                    const ExpertDesc* __restrict__ ex,
+                                    int64_t R, uint16_t* __restrict__ Xb, int8_t* __restrict__ XqA, float* __restrict__ XsA,
+                                    int8_t* __restrict__ XqB, float* __restrict__ XsB) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= R) return;
+  if (row >= v_off[V]) return;  // rows past the last valid route are unused
+  const int v = row_exp[row];
+  const ExpertDesc& E = ex[v];
+  const uint16_t* src = x + (int64_t)row_src[row] * d;
+  for (int b = 0; b < 2; ++b) {
+    const LinDesc& L = E.blk[b];
+    if (b == 1 && E.same_gu) break;
+    if (L.in_slot == 0) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      uint4* d4 = reinterpret_cast<uint4*>(Xb + row * d);
+      for (int i = lane; i < d / 8; i += 32) d4[i] = s4[i];
+    } else {
+      int8_t* q = (L.in_slot == 1 ? XqA : XqB) + row * d;
+      float* sc = (L.in_slot == 1 ? XsA : XsB) + row * (d / 128);
+      const int g = L.a_group == -1 ? d : L.a_group;
+      const int qmax = (1 << (L.a_bits - 1)) - 1;
+      for (int gi = 0; gi < d / g; ++gi) {
+        const float s = quant_group_warp(src + gi * g, q + gi * g, g, qmax, nullptr);
+        if (lane == 0) sc[gi] = s;
+      }
+    }
+  }
+}
+
+// ---- S8: combine, one block per token
+__global__ void combine_kernel(const uint16_t* __restrict__ O, int d, int64_t T, int k, int S,
+                               const int32_t* __restrict__ inv, uint16_t* __restrict__ y) {
+  const int64_t t = blockIdx.x;
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < k; ++j) {
+      const int32_t row = inv[t * k + j];
+      if (row < 0) continue;
+      uint4 v = reinterpret_cast<const uint4*>(O + (int64_t)row * d)[c];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[2 * i] += bf16_bits_to_float(w[i] & 0xFFFFu);
+        acc[2 * i + 1] += bf16_bits_to_float(w[i] >> 16);
+      }
+    }
+    for (int s = 0; s < S; ++s) {
+      uint4 v = reinterpret_cast<const uint4*>(O + (s * T + t) * d)[c];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[2 * i] += bf16_bits_to_float(w[i] & 0xFFFFu);
+        acc[2 * i + 1] += bf16_bits_to_float(w[i] >> 16);
+      }
+    }
+    uint32_t out[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      out[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    reinterpret_cast<uint4*>(y + t * d)[c] = make_uint4(out[0], out[1], out[2], out[3]);
+  }
+}
+
+// ---------------------------------------------------------------- host launchers
+int64_t route_scratch_bytes(int64_t n_routes, int E) {
+  const int64_t nch = (n_routes + kRouteChunk - 1) / kRouteChunk;
+  return ((nch * E * 4) + 255) / 256 * 256;
+}
+
+cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T, int k, int E, int S,
+                              const float* shared_w, int32_t* counts, int32_t* offsets, int32_t* v_off, int32_t* perm,
+                              int32_t* row_src, float* row_w, int32_t* row_exp, int32_t* inv, int32_t* err,
+                              void* scratch, cudaStream_t st) {
+  if (E > 256) return cudaErrorInvalidValue;
+  const int64_t n = T * k;
+  const int nch = (int)((n + kRouteChunk - 1) / kRouteChunk);
+  int32_t* hist = reinterpret_cast<int32_t*>(scratch);
+  if (nch > 0) {
+    route_count_kernel<<<nch, 256, 0, st>>>(ids, n, E, hist, err);
+  }
+  route_scan_kernel<<<1, 256, 0, st>>>(hist, nch, E, S, T, counts, offsets, v_off);
+  if (nch > 0) {
+    route_place_kernel<<<nch, 256, 0, st>>>(ids, topk_w, n, k, E, row_src ? (int64_t)S * T : 0, hist,
+                                            row_src ? nullptr : offsets, v_off, perm, row_src, row_w, row_exp, inv);
+  }
+  if (row_src && S > 0 && T > 0) {
+    route_shared_kernel<<<(unsigned)((T * S + 255) / 256), 256, 0, st>>>(T, E, S, shared_w, row_src, row_w, row_exp);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, const int32_t* row_exp,
+                                const int32_t* v_off, int V,
+                                const ExpertDesc* ex, int64_t R, void* Xb, void* XqA, float* XsA, void* XqB, float* XsB,
+                                cudaStream_t st) {
+  if (R <= 0) return cudaSuccess;
+  gather_quant_kernel<<<(unsigned)((R * 32 + 255) / 256), 256, 0, st>>>(
+      (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const void* O, int d, int64_t T, int k, int S, const int32_t* inv, void* y,
+                           cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  combine_kernel<<<(unsigned)T, 128, 0, st>>>((const uint16_t*)O, d, T, k, S, inv, (uint16_t*)y);
+  return cudaGetLastError();
+}
+
+}  // namespace mxm

@@ -50,6 +50,32 @@ def test_route_prep_conservation_and_topk_e():
         route_prep(np.array([[0, E]]), E)
 
 
+def _bf16_round_exact(v: Fraction) -> Fraction:
+    """Round a rational to the nearest bf16 value (8 significant bits), ties to even — exact arithmetic."""
+    if v == 0:
+        return v
+    sgn = 1 if v > 0 else -1
+    a = abs(v)
+    e = 0
+    while a >= 2:
+        a /= 2
+        e += 1
+    while a < 1:
+        a *= 2
+        e -= 1
+    m = a * 128  # in [128, 256)
+    fl = m.numerator // m.denominator
+    rem = m - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    return sgn * Fraction(fl) * Fraction(2) ** (e - 7)
+
+
+def test_bf16_round_exact_helper():
+    assert _bf16_round_exact(Fraction(257)) == 256 and _bf16_round_exact(Fraction(259)) == 260
+    assert _bf16_round_exact(Fraction(-1, 3)) == Fraction(-171, 512)
+
+
 @pytest.mark.parametrize("sch", [C.WO(4, 64), C.WO(2, 128), C.WO(3, -1, True), C.WO(8, 64)])
 def test_wo_linear_bruteforce(sch):
     rng = np.random.default_rng(1)
@@ -66,7 +92,7 @@ def test_wo_linear_bruteforce(sch):
                 wq = int(blk.codes[n, k]) * Fraction(blk.scale[n, k // g])
                 if blk.zero is not None:
                     wq += Fraction(blk.zero[n, k // g])
-                acc += Fraction(X[m, k]) * wq
+                acc += Fraction(X[m, k]) * _bf16_round_exact(wq)  # reading R5: bf16 dequantized weight
             assert abs(float(acc) - y[m, n]) <= 1e-12 * max(1.0, abs(float(acc)))
 
 
