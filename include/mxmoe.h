@@ -134,6 +134,16 @@ mxm_status mxm_poll_device_error(const mxm_layer* l, const void* workspace, mxm_
 mxm_status mxm_debug_task_stats(const mxm_layer* l, const void* workspace, int64_t T, int32_t top_k,
                                 mxm_stream stream, int32_t* n_tasks, int32_t* n_executed);
 
+/* Profiling (bench / tests): record CUDA events around every launch of the next calls in a ring of
+ * n_slots calls (0 disables). [sync] allocation. */
+mxm_status mxm_layer_profile(mxm_layer* l, int32_t n_slots);
+/* [sync] per-stage device milliseconds of the recorded calls, ms[i*5 + s] for stage s =
+ * route-prep, act-quant+gather, plan, persistent group-GEMM, combine (oldest ring slot first is NOT
+ * guaranteed: slot i = call i mod n_slots). */
+mxm_status mxm_layer_profile_read(mxm_layer* l, float* ms, int32_t n, int32_t* n_recorded);
+/* Number of library kernels one mxm_moe_group_gemm call launches (route x3-4, gather, plan, GEMM, combine). */
+int32_t mxm_kernels_per_call(const mxm_layer* l);
+
 /* Thread-local message for the last error returned on this thread. */
 const char* mxm_last_error(void);
 /* Library version string. */

@@ -200,6 +200,22 @@ class MoELayer:
                                         _ptr(out), _ptr(ws), ws.numel(), _stream()))
         return out
 
+    def profile(self, n_slots: int):
+        """Record per-stage CUDA events for the next calls (ring of n_slots calls)."""
+        check(load().mxm_layer_profile(self._h, n_slots))
+
+    def profile_read(self, n: int):
+        """[n_recorded, 5] stage milliseconds: route, gather, plan, gemm, combine."""
+        import numpy as np
+        buf = (C.c_float * (5 * n))()
+        got = C.c_int32()
+        check(load().mxm_layer_profile_read(self._h, buf, n, C.byref(got)))
+        return np.frombuffer(buf, dtype=np.float32).reshape(n, 5)[: got.value].copy()
+
+    @property
+    def kernels_per_call(self) -> int:
+        return int(load().mxm_kernels_per_call(self._h))
+
     def poll_error(self, workspace: Optional[torch.Tensor] = None) -> int:
         code = C.c_int32()
         ws = workspace if workspace is not None else self._ws

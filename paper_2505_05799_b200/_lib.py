@@ -55,6 +55,9 @@ SIGNATURES = {
     "mxm_moe_group_gemm": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _I64, _P]),
     "mxm_poll_device_error": (C.c_int, [_P, _P, _P, C.POINTER(_I32)]),
     "mxm_debug_task_stats": (C.c_int, [_P, _P, _I64, _I32, _P, C.POINTER(_I32), C.POINTER(_I32)]),
+    "mxm_layer_profile": (C.c_int, [_P, _I32]),
+    "mxm_layer_profile_read": (C.c_int, [_P, _P, _I32, C.POINTER(_I32)]),
+    "mxm_kernels_per_call": (C.c_int32, [_P]),
     "mxm_last_error": (C.c_char_p, []),
     "mxm_version": (C.c_char_p, []),
 }

@@ -80,7 +80,15 @@ struct mxm_layer {
   std::vector<ExpertDesc> ex;
   ExpertDesc* ex_dev;
   bool need_xb, need_xqa, need_xqb, need_hq;
+  // optional per-stage timing: kProfEv events per slot recorded around the launches of a call
+  int prof_n = 0;
+  int64_t prof_calls = 0;
+  std::vector<cudaEvent_t> prof_ev;
+  ~mxm_layer() {
+    for (auto e : prof_ev) cudaEventDestroy(e);
+  }
 };
+static constexpr int kProfEv = 6;  // start | route | gather | plan | gemm | combine
 
 // workspace layout for T tokens, k routes
 struct WsLayout {
@@ -324,17 +332,30 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   int32_t* row_exp = (int32_t*)P(w.row_exp);
   int32_t* inv = (int32_t*)P(w.inv);
 
+  cudaEvent_t* pev = nullptr;
+  if (l->prof_n > 0) {
+    mxm_layer* ml = const_cast<mxm_layer*>(l);
+    pev = &ml->prof_ev[(size_t)(ml->prof_calls % ml->prof_n) * kProfEv];
+    ++ml->prof_calls;
+  }
+  auto mark = [&](int i) {
+    if (pev) cudaEventRecord(pev[i], st);
+  };
+  mark(0);
   MXM_CUDA(cudaMemsetAsync(err, 0, 4, st));
   // S1 route prep
   MXM_CUDA(launch_route_prep(topk_ids, topk_w, T, k, l->E, l->S, shared_w, (int32_t*)P(w.counts), nullptr, v_off,
                              nullptr, row_src, row_w, row_exp, inv, err, P(w.route_scratch), st));
+  mark(1);
   // S2 activation quantize + gather
   MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
                                (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), st));
+  mark(2);
   // S3 plan
   MXM_CUDA(launch_plan(l->ex_dev, l->V, l->E, T, l->d, v_off, (int)w.g_max, w.task_cap, (Task*)P(w.tasks),
                        (int32_t*)P(w.meta), (int32_t*)P(w.grp_n1), (int32_t*)P(w.grp_nq), (int32_t*)P(w.p1_done),
                        (int32_t*)P(w.hq_done), st));
+  mark(3);
   // S4-S7 persistent group GEMM
   GemmParams prm;
   memset(&prm, 0, sizeof(prm));
@@ -366,10 +387,39 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   prm.d = l->d;
   prm.f_max = l->f_max;
   MXM_CUDA(launch_moe_gemm(prm, num_sms(), st));
+  mark(4);
   // S8 combine
   MXM_CUDA(launch_combine(P(w.O), l->d, T, k, l->S, inv, y, st));
+  mark(5);
   return MXM_OK;
 }
+
+mxm_status mxm_layer_profile(mxm_layer* l, int32_t n_slots) {
+  if (!l || n_slots < 0 || n_slots > 100000) return fail(MXM_E_CONFIG, "bad argument");
+  for (auto e : l->prof_ev) cudaEventDestroy(e);
+  l->prof_ev.clear();
+  l->prof_n = 0;
+  l->prof_calls = 0;
+  l->prof_ev.resize((size_t)n_slots * kProfEv);
+  for (auto& e : l->prof_ev) MXM_CUDA(cudaEventCreate(&e));
+  l->prof_n = n_slots;
+  return MXM_OK;
+}
+
+mxm_status mxm_layer_profile_read(mxm_layer* l, float* ms, int32_t n, int32_t* n_recorded) {
+  if (!l || !ms || !n_recorded) return fail(MXM_E_CONFIG, "null argument");
+  const int64_t rec = l->prof_calls < l->prof_n ? l->prof_calls : l->prof_n;
+  const int64_t m = rec < n ? rec : n;
+  for (int64_t i = 0; i < m; ++i) {
+    cudaEvent_t* e = &l->prof_ev[(size_t)i * kProfEv];
+    MXM_CUDA(cudaEventSynchronize(e[kProfEv - 1]));
+    for (int j = 0; j < kProfEv - 1; ++j) MXM_CUDA(cudaEventElapsedTime(&ms[i * (kProfEv - 1) + j], e[j], e[j + 1]));
+  }
+  *n_recorded = (int32_t)m;
+  return MXM_OK;
+}
+
+int32_t mxm_kernels_per_call(const mxm_layer* l) { return l ? 7 + (l->S > 0 ? 1 : 0) : 0; }
 
 mxm_status mxm_poll_device_error(const mxm_layer* l, const void* ws, mxm_stream stream, int32_t* code) {
   if (!l || !ws || !code) return fail(MXM_E_CONFIG, "null argument");
