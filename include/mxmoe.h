@@ -141,6 +141,12 @@ mxm_status mxm_layer_profile(mxm_layer* l, int32_t n_slots);
  * route-prep, act-quant+gather, plan, persistent group-GEMM, combine (oldest ring slot first is NOT
  * guaranteed: slot i = call i mod n_slots). */
 mxm_status mxm_layer_profile_read(mxm_layer* l, float* ms, int32_t n, int32_t* n_recorded);
+/* Debug: accumulate per-CTA cycle counters of the persistent kernel's wait sites into dev_buf
+ * (uint64 [num_SMs][16], caller-zeroed; NULL disables). Slots: 0 producer ring-slot wait, 1 producer
+ * stage-free wait, 2 producer dependency wait, 3-6 MMA waits (task, accumulator, data, transform),
+ * 7-8 transform waits (task, data), 9-10 epilogue waits (task, accumulator), 13 MMA stages issued,
+ * 14 h-quant dependency wait, 15 kernel cycles. */
+mxm_status mxm_layer_debug_counters(mxm_layer* l, void* dev_buf);
 /* Number of library kernels one mxm_moe_group_gemm call launches (route x3-4, gather, plan, GEMM, combine). */
 int32_t mxm_kernels_per_call(const mxm_layer* l);
 

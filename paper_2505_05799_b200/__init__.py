@@ -212,6 +212,10 @@ class MoELayer:
         check(load().mxm_layer_profile_read(self._h, buf, n, C.byref(got)))
         return np.frombuffer(buf, dtype=np.float32).reshape(n, 5)[: got.value].copy()
 
+    def debug_counters(self, buf: Optional[torch.Tensor]):
+        """Attach (or detach with None) a zeroed uint64 device buffer [num_SMs, 16] of wait-site cycle counters."""
+        check(load().mxm_layer_debug_counters(self._h, _ptr(buf)))
+
     @property
     def kernels_per_call(self) -> int:
         return int(load().mxm_kernels_per_call(self._h))

@@ -82,6 +82,7 @@ struct mxm_layer {
   bool need_xb, need_xqa, need_xqb, need_hq;
   // optional per-stage timing: kProfEv events per slot recorded around the launches of a call
   int prof_n = 0;
+  void* prof_counters = nullptr;  // device [grid][16] u64 wait-site cycle counters (debug)
   int64_t prof_calls = 0;
   std::vector<cudaEvent_t> prof_ev;
   ~mxm_layer() {
@@ -94,7 +95,7 @@ static constexpr int kProfEv = 6;  // start | route | gather | plan | gemm | com
 struct WsLayout {
   int64_t R, g_max, task_cap;
   int64_t err, route_scratch, counts, v_off, row_src, row_w, row_exp, inv;
-  int64_t Xb, XqA, XsA, XqB, XsB, H, Hq, Hs, O;
+  int64_t Xb, XqA, XsA, XqB, XsB, H, Hq, Hs, hmax, O;
   int64_t tasks, meta, grp_n1, grp_nq, p1_done, hq_done;
   int64_t total;
 };
@@ -127,6 +128,7 @@ static WsLayout make_layout(const mxm_layer* l, int64_t T, int k) {
   w.H = take(2 * R * l->f_max);
   w.Hq = l->need_hq ? take(R * l->f_max) : -1;
   w.Hs = l->need_hq ? take(4 * R * (l->f_max / 128)) : -1;
+  w.hmax = l->need_hq ? take(4 * R) : -1;
   w.O = take(2 * R * l->d);
   w.tasks = take(16 * w.task_cap);
   w.meta = take(4 * (8 + 4 * w.g_max));
@@ -276,8 +278,6 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
     }
     const mxm_scheme& sg = d->blocks[v * 3 + 0].scheme;
     const mxm_scheme& su = d->blocks[v * 3 + 1].scheme;
-    e.same_gu = sg.w_bits == su.w_bits && sg.a_bits == su.a_bits && sg.w_group == su.w_group &&
-                (sg.a_bits == 16 ? 1 : sg.a_group == su.a_group) && (sg.symmetric != 0) == (su.symmetric != 0);
     // input slots
     const bool gwa = sg.a_bits != 16, uwa = su.a_bits != 16;
     e.blk[0].in_slot = gwa ? 1 : 0;
@@ -288,6 +288,10 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
     else
       e.blk[1].in_slot = gwa ? 2 : 1;
     e.blk[2].in_slot = d->blocks[v * 3 + 2].scheme.a_bits != 16 ? 1 : 0;
+    // gate and up share one K loop (and the token tile) when they use the same MMA kind and input:
+    // any two bf16-kind blocks (w16 / weight-only of any bits and group), or identical W-A schemes
+    e.dual = (!gwa && !uwa) || (gwa && uwa && e.blk[1].in_slot == 1 && sg.w_bits == su.w_bits &&
+                                sg.w_group == su.w_group);
     for (int j = 0; j < 2; ++j) {
       if (e.blk[j].in_slot == 0) l->need_xb = true;
       if (e.blk[j].in_slot == 1) l->need_xqa = true;
@@ -349,7 +353,7 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   mark(1);
   // S2 activation quantize + gather
   MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
-                               (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), st));
+                               (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), (uint32_t*)P(w.hmax), st));
   mark(2);
   // S3 plan
   MXM_CUDA(launch_plan(l->ex_dev, l->V, l->E, T, l->d, v_off, (int)w.g_max, w.task_cap, (Task*)P(w.tasks),
@@ -382,10 +386,12 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   prm.H = (uint16_t*)P(w.H);
   prm.Hq = (int8_t*)P(w.Hq);
   prm.Hs = (float*)P(w.Hs);
+  prm.hmax = (uint32_t*)P(w.hmax);
   prm.O = (uint16_t*)P(w.O);
   prm.row_w = row_w;
   prm.d = l->d;
   prm.f_max = l->f_max;
+  prm.prof = reinterpret_cast<unsigned long long*>(l->prof_counters);
   MXM_CUDA(launch_moe_gemm(prm, num_sms(), st));
   mark(4);
   // S8 combine
@@ -416,6 +422,12 @@ mxm_status mxm_layer_profile_read(mxm_layer* l, float* ms, int32_t n, int32_t* n
     for (int j = 0; j < kProfEv - 1; ++j) MXM_CUDA(cudaEventElapsedTime(&ms[i * (kProfEv - 1) + j], e[j], e[j + 1]));
   }
   *n_recorded = (int32_t)m;
+  return MXM_OK;
+}
+
+mxm_status mxm_layer_debug_counters(mxm_layer* l, void* dev_buf) {
+  if (!l) return fail(MXM_E_CONFIG, "null layer");
+  l->prof_counters = dev_buf;
   return MXM_OK;
 }
 

@@ -56,7 +56,7 @@ struct LinDesc {
 struct ExpertDesc {
   LinDesc blk[3];
   int32_t inter;      // f of this expert
-  int32_t same_gu;    // gate and up share the scheme (one sub-loop, shared B tile)
+  int32_t dual;       // gate and up run as one K loop sharing the token tile (same MMA kind and input slot)
   int32_t shared;     // 1 = shared expert (all tokens)
   int32_t pad;
 };

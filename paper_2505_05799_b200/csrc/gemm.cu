@@ -10,8 +10,8 @@
 //   phase 2: down, epilogue o * w_e -> bf16 (Eq. 2)
 // Warp roles ("micro-kernels ... CTA-index independent", "same number of warps"):
 //   warp 0      producer: queue pop, dependency wait, bulk copy of packed weight chunks, TMA of tokens
-//   warp 1      MMA issuer: tcgen05.mma kind::f16 (weight-only / bf16) or kind::i8 (weight-activation)
-//   warp 2      TMEM allocator (512 columns = 4 accumulator buffers of 128 columns)
+//   warp 1      TMEM allocator (512 columns = 4 accumulator buffers of 128 columns) and MMA issuer:
+//               tcgen05.mma kind::f16 (weight-only / bf16) or kind::i8 (weight-activation)
 //   warps 4-7   transform: packed codes -> bf16 (dequant, weight-only) or s8 (w4/w5 unpack) A tiles
 //   warps 8-15  epilogue (2 warpgroups split the token columns): TMEM -> scales -> SwiGLU / w_e -> HBM
 // Weight-activation g128 blocks drain the int32 accumulator every 128-K group (the group scales
@@ -30,7 +30,8 @@ namespace mxm {
 constexpr int kStages = 3;
 constexpr int kRing = 4;
 constexpr int kAccBufs = 4;
-constexpr int kThreads = 512;
+constexpr int kThreads = 512;  // 16 warps: producer, 2 MMA issuers, idle, 4 transform, 8 epilogue
+constexpr int kXfWarps = 4;     // transform warps 4..7 (one A row per thread)
 constexpr int kRawBytes = 10752;
 constexpr int kTileBytes = 16384;
 
@@ -38,7 +39,7 @@ constexpr int kOffA = 0;
 constexpr int kOffB = kOffA + kStages * 2 * kTileBytes;
 constexpr int kOffRaw = kOffB + kStages * kTileBytes;
 constexpr int kOffCtl = kOffRaw + kStages * 2 * kRawBytes;
-constexpr int kCtlBytes = 512;
+constexpr int kCtlBytes = 1024;
 constexpr int kSmemBytes = kOffCtl + kCtlBytes + 1024;
 
 struct Ctl {
@@ -47,12 +48,13 @@ struct Ctl {
   uint64_t tfull[kRing], tempty[kRing];
   Task ring[kRing];
   uint32_t tmem_base;
+  uint32_t colmax[2][2][4][8];  // [buffer][warpgroup][lane quarter][column] for the fused g128 h-quant
 };
 static_assert(sizeof(Ctl) <= kCtlBytes, "ctl");
 
 struct SubLoop {
   const LinDesc* mat[2];
-  int nmats, bmap, ns, i8, xform, g128;
+  int nmats, bmap, ns, i8, xform, g128;  // xform: bit m set = mat m needs the packed->A transform
 };
 
 __device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, int bmap) {
@@ -63,7 +65,7 @@ __device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, i
   s.bmap = bmap;
   s.ns = a->geo.ns;
   s.i8 = kind_is_i8(a->geo.kind);
-  s.xform = kind_needs_transform(a->geo.kind);
+  s.xform = (kind_needs_transform(a->geo.kind) ? 1 : 0) | ((b && kind_needs_transform(b->geo.kind)) ? 2 : 0);
   s.g128 = s.i8 && a->geo.group == 128;
   return s;
 }
@@ -71,7 +73,7 @@ __device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, i
 __device__ __forceinline__ int build_subloops(const Task& t, const ExpertDesc* __restrict__ ex, SubLoop* sl) {
   const ExpertDesc& e = ex[t.expert];
   if (t.phase == 0) {
-    if (e.same_gu) {
+    if (e.dual) {
       sl[0] = make_sl(&e.blk[0], &e.blk[1], e.blk[0].in_slot);
       return 1;
     }
@@ -102,26 +104,27 @@ __device__ __forceinline__ uint32_t deq_pair(uint32_t fields, uint32_t off2, uin
   return bf2_fma(bf2_sub(fields | 0x43004300u, off2), s2, z2);
 }
 
-__device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_t* __restrict__ A, const PackGeom& g,
-                                         int ks, int r, uint32_t& s2, uint32_t& z2) {
+// Weight-only dequant of one A row (thread r = row r): packed codes -> bf16 q*s + z, swizzled store.
+// `hm`: this stage starts a group, so the chunk begins with scale[128] (and zero[128] if asymmetric).
+template <int BITS>
+__device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_t* __restrict__ A, bool hm,
+                                         int meta_bytes, bool sym, uint32_t off2, int r, uint32_t& s2, uint32_t& z2) {
   const uint8_t* codes = raw;
-  if (chunk_has_meta(g, ks)) {
+  if (hm) {
     const uint32_t sb = reinterpret_cast<const uint16_t*>(raw)[r];
     s2 = sb | (sb << 16);
-    if (!g.sym) {
+    if (!sym) {
       const uint32_t zb = reinterpret_cast<const uint16_t*>(raw + 256)[r];
       z2 = zb | (zb << 16);
     } else {
       z2 = 0;
     }
-    codes += g.meta_bytes;
+    codes += meta_bytes;
   }
   const uint32_t* w = reinterpret_cast<const uint32_t*>(codes);
   uint8_t* dst = A + r * 128;
   const int sw = r & 7;
-  const uint32_t off = g.sym ? (1u << (g.w_bits - 1)) : 0u;
-  const uint32_t off2 = (0x4300u | off) * 0x10001u;
-  if (g.w_bits == 4) {
+  if constexpr (BITS == 4) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t word = w[j * 128 + r];
@@ -132,7 +135,7 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_
       o.w = deq_pair((word >> 12) & 0x000F000Fu, off2, s2, z2);
       *reinterpret_cast<uint4*>(dst + ((j ^ sw) << 4)) = o;
     }
-  } else if (g.w_bits == 2) {
+  } else if constexpr (BITS == 2) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t word = w[j * 128 + r];
@@ -148,7 +151,7 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_
       *reinterpret_cast<uint4*>(dst + (((2 * j) ^ sw) << 4)) = o0;
       *reinterpret_cast<uint4*>(dst + (((2 * j + 1) ^ sw) << 4)) = o1;
     }
-  } else if (g.w_bits == 3) {
+  } else if constexpr (BITS == 3) {
     const uint32_t* wh = w + 4 * 128;
     const uint32_t h0 = wh[r], h1 = wh[128 + r];
 #pragma unroll
@@ -163,8 +166,9 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_
       *reinterpret_cast<uint4*>(dst + (((2 * j + 1) ^ sw) << 4)) = make_uint4(p[4], p[5], p[6], p[7]);
     }
   } else {  // 8-bit: fp32 path (128 + u is not exact in bf16 for u >= 128)
-    const float sf = __uint_as_float(s2 << 16), zf = __uint_as_float(z2 << 16), fo = (float)off;
-#pragma unroll 4
+    const float sf = __uint_as_float(s2 << 16), zf = __uint_as_float(z2 << 16);
+    const float fo = (float)((off2 & 0xFFu));
+#pragma unroll
     for (int c = 0; c < 8; ++c) {
       uint32_t o[4];
 #pragma unroll
@@ -183,14 +187,32 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_
   }
 }
 
+__device__ __forceinline__ void xform_wo_any(int bits, const uint8_t* raw, uint8_t* A, bool hm, int mb, bool sym,
+                                             uint32_t off2, int r, uint32_t& s2, uint32_t& z2) {
+  switch (bits) {
+    case 2:
+      xform_wo<2>(raw, A, hm, mb, sym, off2, r, s2, z2);
+      break;
+    case 3:
+      xform_wo<3>(raw, A, hm, mb, sym, off2, r, s2, z2);
+      break;
+    case 4:
+      xform_wo<4>(raw, A, hm, mb, sym, off2, r, s2, z2);
+      break;
+    default:
+      xform_wo<8>(raw, A, hm, mb, sym, off2, r, s2, z2);
+      break;
+  }
+}
+
 __device__ __forceinline__ uint32_t to_s8_4(uint32_t u, uint32_t bias) { return (u + bias) ^ 0x80808080u; }
 
-__device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, uint8_t* __restrict__ A, const PackGeom& g,
-                                         int r) {
+template <int BITS>
+__device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, uint8_t* __restrict__ A, int r) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(raw);
   uint8_t* dst = A + r * 128;
   const int sw = r & 7;
-  if (g.w_bits == 4) {
+  if constexpr (BITS == 4) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const uint32_t w0 = w[(2 * c) * 128 + r], w1 = w[(2 * c + 1) * 128 + r];
@@ -232,6 +254,216 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
   return *reinterpret_cast<uint16_t*>(&h);
 }
 
+// broadcast the per-column value preloaded by lane (idx & 31) of register lo (idx < 32) / hi
+__device__ __forceinline__ float colval(float lo, float hi, int idx) {
+  return __shfl_sync(0xffffffffu, idx < 32 ? lo : hi, idx & 31);
+}
+
+// packed fp32x2 helpers (sm_100a FFMA2 / FMUL2 / FADD2)
+__device__ __forceinline__ unsigned long long f2u(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 u2f(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+
+// One drain event of the register-accumulating epilogue for HALF token columns of this warpgroup.
+// acc2 holds 64 fp32 accumulators as 32 pairs: dual gate/up -> gate cols in pairs [0,16), up in [16,32);
+// single -> cols in pairs [0,32). i8: acc += int32 * (s_w * s_a[col]) ; bf16-kind: acc += fp32.
+template <int HALF, int DST0>
+__device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8, bool two,
+                                            float sw0, float sw1, float sa_lo, float sa_hi) {
+  constexpr int CH = 8;
+#pragma unroll
+  for (int c0 = 0; c0 < HALF; c0 += CH) {
+    uint32_t va[16], vb[16];
+    if constexpr (CH == 16) {
+      tmem_ld16(addrA + c0, va);
+      if (two) tmem_ld16(addrB + c0, vb);
+    } else {
+      uint32_t (&va8)[8] = *reinterpret_cast<uint32_t(*)[8]>(&va[0]);
+      uint32_t (&vb8)[8] = *reinterpret_cast<uint32_t(*)[8]>(&vb[0]);
+      tmem_ld8(addrA + c0, va8);
+      if (two) tmem_ld8(addrB + c0, vb8);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < CH; j += 2) {
+      const int col = c0 + j;
+      if (i8) {
+        const float2 sa = make_float2(colval(sa_lo, sa_hi, col), colval(sa_lo, sa_hi, col + 1));
+        const float2 fa = make_float2((float)(int32_t)va[j], (float)(int32_t)va[j + 1]);
+        acc2[DST0 + col / 2] = ffma2(fa, fmul2(make_float2(sw0, sw0), sa), acc2[DST0 + col / 2]);
+        if (two) {
+          const float2 fb = make_float2((float)(int32_t)vb[j], (float)(int32_t)vb[j + 1]);
+          acc2[16 + col / 2] = ffma2(fb, fmul2(make_float2(sw1, sw1), sa), acc2[16 + col / 2]);
+        }
+      } else {
+        acc2[DST0 + col / 2] = fadd2(acc2[DST0 + col / 2], make_float2(__uint_as_float(va[j]), __uint_as_float(va[j + 1])));
+        if (two)
+          acc2[16 + col / 2] = fadd2(acc2[16 + col / 2], make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1])));
+      }
+    }
+  }
+}
+
+template <int DST0>
+__device__ __forceinline__ void drain_event_any(int half, float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8,
+                                                bool two, float sw0, float sw1, float sa_lo, float sa_hi) {
+  switch (half) {
+    case 8:
+      drain_event<8, DST0>(acc2, addrA, addrB, i8, two, sw0, sw1, sa_lo, sa_hi);
+      break;
+    case 16:
+      drain_event<16, DST0>(acc2, addrA, addrB, i8, two, sw0, sw1, sa_lo, sa_hi);
+      break;
+    case 32:
+      drain_event<32, DST0>(acc2, addrA, addrB, i8, two, sw0, sw1, sa_lo, sa_hi);
+      break;
+    default:
+      if constexpr (DST0 == 0) drain_event<64, 0>(acc2, addrA, addrB, i8, false, sw0, sw1, sa_lo, sa_hi);
+      break;
+  }
+}
+
+// h for 8 token columns [colc, colc+8) of output channel n (= this thread's TMEM lane) in the form the
+// down block consumes (dmode): 0 bf16 H (weight-only / bf16 down); 1 bf16 H + row max|h| via atomicMax
+// (per-token W-A down, quantized later in one pass); 2 fused per-128-group quantization: the group is
+// exactly this tile's 128 channels, so codes + scale are produced here (DESIGN R9).
+__device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int dmode, int qmax, int n, int colc,
+                                        const float (&h)[8], Ctl& ctl, int wg, int q, int lane, uint32_t& rbuf) {
+  float hf[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) hf[j] = bf16f(f2bf(h[j]));  // h is defined in bf16 (DESIGN R16)
+  if (dmode == 2) {
+    uint32_t m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(hf[j])));
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ctl.colmax[rbuf][wg][q][j] = m[j];
+    named_bar_sync(2 + wg, 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t a = max(max(ctl.colmax[rbuf][wg][0][j], ctl.colmax[rbuf][wg][1][j]),
+                             max(ctl.colmax[rbuf][wg][2][j], ctl.colmax[rbuf][wg][3][j]));
+      const float amax = __uint_as_float(a), fq = (float)qmax;
+      const float r = amax > 0.f ? __fdiv_rn(fq, amax) : 0.f;
+      const float sc = amax > 0.f ? __fdiv_rn(amax, fq) : 1.f;
+      const int col = colc + j;
+      if (col < t.rows) {
+        const int64_t row = (int64_t)t.row0 + col;
+        const float qv = fminf(fmaxf(rintf(__fmul_rn(hf[j], r)), -fq), fq);
+        p.Hq[row * p.f_max + n] = (int8_t)(int)qv;
+        if (q == 0 && lane == 0) p.Hs[row * (p.f_max / 128) + t.ntile] = sc;
+      }
+    }
+    rbuf ^= 1;
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int col = colc + j;
+    if (col < t.rows) p.H[((int64_t)t.row0 + col) * p.f_max + n] = f2bf(hf[j]);
+  }
+  if (dmode == 1) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(hf[j])));
+      const int col = colc + j;
+      if (lane == 0 && col < t.rows) atomicMax(p.hmax + t.row0 + col, m);
+    }
+  }
+}
+
+// wait with optional cycle accounting (debug profiling of the stage pipeline)
+__device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned long long& acc, bool on) {
+  if (!on) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const unsigned long long t0 = clock64();
+  mbar_wait(bar, parity);
+  acc += clock64() - t0;
+}
+
+struct MmaState {
+  uint32_t stage, sphase, abuf, acc_ph, ar_ph;
+};
+
+// One sub-loop of MMAs (all K stages of one or two mats sharing the token tile), specialised on the MMA
+// kind and the number of mats so the issue loop has no runtime kind branches.
+template <bool I8, bool TWO, int ROLE>
+__device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tmem, const SubLoop& s, uint32_t nt,
+                                            MmaState& st, unsigned long long (&pc)[16], bool prof_on) {
+  const bool nbuf2 = TWO && !s.g128;
+  const uint32_t idesc = I8 ? idesc_s8(nt) : idesc_bf16(nt);
+  const uint32_t a_base = smem_u32(smem + kOffA), b_base = smem_u32(smem + kOffB);
+  uint32_t b0 = 0, b1 = 0;
+  for (int ks = 0; ks < s.ns; ++ks) {
+    const bool ev_start = s.g128 || ks == 0, ev_end = s.g128 || ks == s.ns - 1;
+    if (ev_start) {
+      b0 = st.abuf;
+      twait(&ctl.acce[b0], ((st.acc_ph >> b0) & 1) ^ 1, pc[4], prof_on);
+      st.acc_ph ^= 1u << b0;
+      st.abuf = (st.abuf + 1) & (kAccBufs - 1);
+      if (nbuf2) {
+        b1 = st.abuf;
+        twait(&ctl.acce[b1], ((st.acc_ph >> b1) & 1) ^ 1, pc[4], prof_on);
+        st.acc_ph ^= 1u << b1;
+        st.abuf = (st.abuf + 1) & (kAccBufs - 1);
+      }
+    }
+    const uint32_t stage = st.stage;
+    twait(&ctl.full[stage], st.sphase, pc[5], prof_on);
+    if (s.xform) {
+      twait(&ctl.aready[stage], (st.ar_ph >> stage) & 1, pc[6], prof_on);
+      st.ar_ph ^= 1u << stage;
+    }
+    tc_fence_after();
+    const uint32_t bb = b_base + stage * kTileBytes;
+    const uint32_t a0 = a_base + (stage * 2) * kTileBytes, a1 = a0 + kTileBytes;
+    const uint32_t d0 = tmem + b0 * 128u;
+    const uint32_t d1 = nbuf2 ? tmem + b1 * 128u : tmem + b0 * 128u + 64u;
+    const uint32_t acc0 = ev_start ? 0u : 1u;
+    // ROLE 0 (warp 1) issues mat 0 (gate / the single block); ROLE 1 (warp 2) issues mat 1 (up), so each
+    // warp's barrier / commit latency is covered by the other warp's MMAs (the tcgen05 issue queue is shallow)
+    if constexpr (ROLE == 0 || TWO) {
+      const uint32_t dd = ROLE == 0 ? d0 : d1;
+      const uint32_t aa = ROLE == 0 ? a0 : a1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t acc = k == 0 ? acc0 : 1u;
+        if constexpr (I8)
+          mma_i8(dd, sw128_kmajor_desc(aa + k * 32), sw128_kmajor_desc(bb + k * 32), idesc, acc);
+        else
+          mma_bf16(dd, sw128_kmajor_desc(aa + k * 32), sw128_kmajor_desc(bb + k * 32), idesc, acc);
+      }
+    }
+    mma_commit(&ctl.empty[stage]);
+    if (prof_on) pc[13] += 1;
+    if (ev_end) {
+      mma_commit(&ctl.accf[b0]);
+      if (nbuf2) mma_commit(&ctl.accf[b1]);
+    }
+    if (++st.stage == kStages) {
+      st.stage = 0;
+      st.sphase ^= 1;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -245,20 +477,20 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&ctl.full[i], 1);
-      mbar_init(&ctl.empty[i], 1);
-      mbar_init(&ctl.aready[i], 4);
+      mbar_init(&ctl.empty[i], 2);  // both MMA warps commit every stage
+      mbar_init(&ctl.aready[i], kXfWarps);
     }
     for (int i = 0; i < kAccBufs; ++i) {
-      mbar_init(&ctl.accf[i], 1);
+      mbar_init(&ctl.accf[i], 2);  // both MMA warps commit at every drain event
       mbar_init(&ctl.acce[i], 8);
     }
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&ctl.tfull[i], 1);
-      mbar_init(&ctl.tempty[i], 13);
+      mbar_init(&ctl.tempty[i], 2 + kXfWarps + 8);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<512>(&ctl.tmem_base);
+  if (warp == 1) tmem_alloc<512>(&ctl.tmem_base);
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 5; ++i)
       for (int j = 0; j < 4; ++j) prefetch_tmap(&p.tmap[i][j]);
@@ -268,6 +500,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = ctl.tmem_base;
   const int n_tasks = p.meta[0];
+  const bool prof_on = p.prof != nullptr;
+  unsigned long long pc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) pc[i] = 0;
+  const unsigned long long t_start = clock64();
 
   if (warp == 0) {
     // =========================== producer
@@ -282,41 +519,56 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         } else {
           t.phase = 255;
         }
-        mbar_wait(&ctl.tempty[slot], rphase ^ 1);
+        twait(&ctl.tempty[slot], rphase ^ 1, pc[0], prof_on);
         ctl.ring[slot] = t;
         mbar_arrive(&ctl.tfull[slot]);
         if (t.phase == 255) break;
         if (t.phase == 1) continue;
         if (t.phase == 2) {
           const ExpertDesc& e = p.ex[t.expert];
-          const bool wa = kind_is_i8(e.blk[2].geo.kind);
-          const int* ctr = (wa ? p.hq_done : p.p1_done) + t.gid;
-          const int need = wa ? p.grp_nq[t.gid] : p.grp_n1[t.gid];
+          // per-token W-A downs wait for the h-quant pass; all others only for the gate/up tiles
+          const bool wa_pt = kind_is_i8(e.blk[2].geo.kind) && e.blk[2].geo.group != 128;
+          const int* ctr = (wa_pt ? p.hq_done : p.p1_done) + t.gid;
+          const int need = wa_pt ? p.grp_nq[t.gid] : p.grp_n1[t.gid];
+          const unsigned long long td = prof_on ? clock64() : 0ull;
           while (ld_acquire_gpu(ctr) < need) __nanosleep(64);
+          if (prof_on) pc[2] += clock64() - td;
           fence_proxy_async_global();
         }
         SubLoop sl[2];
         const int nsl = build_subloops(t, p.ex, sl);
         const int nti = nt_index(t.nt);
         for (int si = 0; si < nsl; ++si) {
-          const SubLoop& s = sl[si];
+          const SubLoop s = sl[si];
           const CUtensorMap* map = &p.tmap[s.bmap][nti];
+          // per-mat chunk streams (gate and up may differ in bits / group / format)
+          const PackGeom& g0 = s.mat[0]->geo;
+          const PackGeom& g1 = s.mat[s.nmats - 1]->geo;
+          const uint32_t cb0 = (uint32_t)g0.code_bytes, mb0 = (uint32_t)g0.meta_bytes;
+          const uint32_t cb1 = (uint32_t)g1.code_bytes, mb1 = (uint32_t)g1.meta_bytes;
+          const int gst0 = g0.group / g0.ks, gst1 = g1.group / g1.ks;
+          const uint8_t* src0 = s.mat[0]->packed + (int64_t)t.ntile * g0.rb_bytes;
+          const uint8_t* src1 = s.nmats == 2 ? s.mat[1]->packed + (int64_t)t.ntile * g1.rb_bytes : nullptr;
+          uint8_t* const dst0 = (s.xform & 1) ? tileRaw(0, 0) : tileA(0, 0);
+          uint8_t* const dst1 = (s.xform & 2) ? tileRaw(0, 1) : tileA(0, 1);
+          const int str0 = (s.xform & 1) ? 2 * kRawBytes : 2 * kTileBytes;
+          const int str1 = (s.xform & 2) ? 2 * kRawBytes : 2 * kTileBytes;
+          const int kstep = s.i8 ? 128 : 64;
+          int gc0 = 0, gc1 = 0;
           for (int ks = 0; ks < s.ns; ++ks) {
-            mbar_wait(&ctl.empty[stage], sphase ^ 1);
-            uint32_t bytes = (uint32_t)t.nt * 128u;
-            uint32_t cb[2];
-            for (int m = 0; m < s.nmats; ++m) {
-              const PackGeom& g = s.mat[m]->geo;
-              cb[m] = (uint32_t)g.code_bytes + (chunk_has_meta(g, ks) ? (uint32_t)g.meta_bytes : 0u);
-              bytes += cb[m];
+            const uint32_t c0 = cb0 + (gc0 == 0 ? mb0 : 0u);
+            const uint32_t c1 = src1 ? cb1 + (gc1 == 0 ? mb1 : 0u) : 0u;
+            if (++gc0 == gst0) gc0 = 0;
+            if (++gc1 == gst1) gc1 = 0;
+            twait(&ctl.empty[stage], sphase ^ 1, pc[1], prof_on);
+            mbar_arrive_expect_tx(&ctl.full[stage], (uint32_t)t.nt * 128u + c0 + c1);
+            bulk_load(dst0 + stage * str0, src0, c0, &ctl.full[stage]);
+            src0 += c0;
+            if (src1) {
+              bulk_load(dst1 + stage * str1, src1, c1, &ctl.full[stage]);
+              src1 += c1;
             }
-            mbar_arrive_expect_tx(&ctl.full[stage], bytes);
-            for (int m = 0; m < s.nmats; ++m) {
-              const LinDesc& L = *s.mat[m];
-              const uint8_t* src = L.packed + chunk_offset(L.geo, t.ntile, ks);
-              bulk_load(s.xform ? tileRaw(stage, m) : tileA(stage, m), src, cb[m], &ctl.full[stage]);
-            }
-            tma_load_2d(tileB(stage), map, &ctl.full[stage], ks * (s.i8 ? 128 : 64), t.row0);
+            tma_load_2d(tileB(stage), map, &ctl.full[stage], ks * kstep, t.row0);
             if (++stage == kStages) {
               stage = 0;
               sphase ^= 1;
@@ -326,15 +578,15 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    // =========================== MMA issuer
+  } else if (warp == 1 || warp == 2) {
+    // =========================== MMA issuers (warp 1: mat 0, warp 2: mat 1)
     if (lane == 0) {
       uint32_t stage = 0, sphase = 0, abuf = 0;
-      uint32_t acc_uses[kAccBufs] = {0, 0, 0, 0};
-      uint32_t ar_uses[kStages] = {0, 0, 0};
+      uint32_t acc_ph = 0;  // bit b: parity of the next wait on acce[b] (phase bits, no local arrays)
+      uint32_t ar_ph = 0;   // bit s: parity of the next wait on aready[s]
       for (uint32_t it = 0;; ++it) {
         const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
-        mbar_wait(&ctl.tfull[slot], rphase);
+        twait(&ctl.tfull[slot], rphase, pc[3], prof_on);
         const Task t = ctl.ring[slot];
         mbar_arrive(&ctl.tempty[slot]);
         if (t.phase == 255) break;
@@ -342,61 +594,36 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         SubLoop sl[2];
         const int nsl = build_subloops(t, p.ex, sl);
         for (int si = 0; si < nsl; ++si) {
-          const SubLoop& s = sl[si];
-          const int nbuf = (s.nmats == 2 && !s.g128) ? 2 : 1;
-          const uint32_t idesc = s.i8 ? idesc_s8(t.nt) : idesc_bf16(t.nt);
-          uint32_t bufs[2] = {0, 0};
-          for (int ks = 0; ks < s.ns; ++ks) {
-            const bool ev_start = s.g128 || ks == 0, ev_end = s.g128 || ks == s.ns - 1;
-            if (ev_start) {
-              for (int b = 0; b < nbuf; ++b) {
-                bufs[b] = abuf;
-                mbar_wait(&ctl.acce[abuf], (acc_uses[abuf] & 1) ^ 1);
-                ++acc_uses[abuf];
-                abuf = (abuf + 1) % kAccBufs;
-              }
-            }
-            mbar_wait(&ctl.full[stage], sphase);
-            if (s.xform) {
-              mbar_wait(&ctl.aready[stage], ar_uses[stage] & 1);
-              ++ar_uses[stage];
-            }
-            tc_fence_after();
-            const uint32_t bbase = smem_u32(tileB(stage));
-            for (int m = 0; m < s.nmats; ++m) {
-              const uint32_t col = nbuf == 2 ? bufs[m] * 128u : bufs[0] * 128u + (uint32_t)m * 64u;
-              const uint32_t abase = smem_u32(tileA(stage, m));
-              const bool first = s.g128 || ks == 0;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint64_t ad = sw128_kmajor_desc(abase + k * 32);
-                const uint64_t bd = sw128_kmajor_desc(bbase + k * 32);
-                const uint32_t acc = (first && k == 0) ? 0u : 1u;
-                if (s.i8)
-                  mma_i8(tmem + col, ad, bd, idesc, acc);
-                else
-                  mma_bf16(tmem + col, ad, bd, idesc, acc);
-              }
-            }
-            mma_commit(&ctl.empty[stage]);
-            if (ev_end)
-              for (int b = 0; b < nbuf; ++b) mma_commit(&ctl.accf[bufs[b]]);
-            if (++stage == kStages) {
-              stage = 0;
-              sphase ^= 1;
-            }
+          const SubLoop s = sl[si];
+          MmaState st{stage, sphase, abuf, acc_ph, ar_ph};
+          const uint32_t nt = t.nt;
+          if (s.i8) {
+            if (s.nmats == 2)
+              (warp == 1 ? mma_subloop<true, true, 0>(ctl, smem, tmem, s, nt, st, pc, prof_on) : mma_subloop<true, true, 1>(ctl, smem, tmem, s, nt, st, pc, prof_on));
+            else
+              (warp == 1 ? mma_subloop<true, false, 0>(ctl, smem, tmem, s, nt, st, pc, prof_on) : mma_subloop<true, false, 1>(ctl, smem, tmem, s, nt, st, pc, prof_on));
+          } else {
+            if (s.nmats == 2)
+              (warp == 1 ? mma_subloop<false, true, 0>(ctl, smem, tmem, s, nt, st, pc, prof_on) : mma_subloop<false, true, 1>(ctl, smem, tmem, s, nt, st, pc, prof_on));
+            else
+              (warp == 1 ? mma_subloop<false, false, 0>(ctl, smem, tmem, s, nt, st, pc, prof_on) : mma_subloop<false, false, 1>(ctl, smem, tmem, s, nt, st, pc, prof_on));
           }
+          stage = st.stage;
+          sphase = st.sphase;
+          abuf = st.abuf;
+          acc_ph = st.acc_ph;
+          ar_ph = st.ar_ph;
         }
       }
     }
     __syncwarp();
   } else if (warp >= 4 && warp < 8) {
-    // =========================== transform warpgroup
+    // =========================== transform warpgroup: one A row per thread, both mats of the stage
     const int r = threadIdx.x - 128;
     uint32_t stage = 0, sphase = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
-      mbar_wait(&ctl.tfull[slot], rphase);
+      twait(&ctl.tfull[slot], rphase, pc[7], prof_on);
       const Task t = ctl.ring[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl.tempty[slot]);
@@ -405,17 +632,36 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       SubLoop sl[2];
       const int nsl = build_subloops(t, p.ex, sl);
       for (int si = 0; si < nsl; ++si) {
-        const SubLoop& s = sl[si];
-        uint32_t s2[2] = {0, 0}, z2[2] = {0, 0};
+        const SubLoop s = sl[si];
+        const bool two = s.nmats == 2;
+        const PackGeom& ga = s.mat[0]->geo;
+        const PackGeom& gb = s.mat[s.nmats - 1]->geo;
+        const int bitsA = ga.w_bits, bitsB = gb.w_bits;
+        const bool symA = ga.sym != 0, symB = gb.sym != 0;
+        const int mbA = ga.meta_bytes, mbB = gb.meta_bytes;
+        const int gstA = ga.group / ga.ks, gstB = gb.group / gb.ks;
+        const uint32_t offA = (0x4300u | (symA ? (1u << (bitsA - 1)) : 0u)) * 0x10001u;
+        const uint32_t offB = (0x4300u | (symB ? (1u << (bitsB - 1)) : 0u)) * 0x10001u;
+        const bool xa = (s.xform & 1) != 0, xb = two && (s.xform & 2) != 0;
+        uint32_t sa = 0, za = 0, sb = 0, zb = 0;
+        int gca = 0, gcb = 0;
         for (int ks = 0; ks < s.ns; ++ks) {
+          const bool hmA = gca == 0, hmB = gcb == 0;
+          if (++gca == gstA) gca = 0;
+          if (++gcb == gstB) gcb = 0;
           if (s.xform) {
-            mbar_wait(&ctl.full[stage], sphase);
-            for (int m = 0; m < s.nmats; ++m) {
-              const PackGeom& g = s.mat[m]->geo;
-              if (s.i8)
-                xform_wa(tileRaw(stage, m), tileA(stage, m), g, r);
-              else
-                xform_wo(tileRaw(stage, m), tileA(stage, m), g, ks, r, s2[m], z2[m]);
+            twait(&ctl.full[stage], sphase, pc[8], prof_on);
+            if (s.i8) {
+              if (bitsA == 4) {
+                if (xa) xform_wa<4>(tileRaw(stage, 0), tileA(stage, 0), r);
+                if (xb) xform_wa<4>(tileRaw(stage, 1), tileA(stage, 1), r);
+              } else {
+                if (xa) xform_wa<5>(tileRaw(stage, 0), tileA(stage, 0), r);
+                if (xb) xform_wa<5>(tileRaw(stage, 1), tileA(stage, 1), r);
+              }
+            } else {
+              if (xa) xform_wo_any(bitsA, tileRaw(stage, 0), tileA(stage, 0), hmA, mbA, symA, offA, r, sa, za);
+              if (xb) xform_wo_any(bitsB, tileRaw(stage, 1), tileA(stage, 1), hmB, mbB, symB, offB, r, sb, zb);
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -432,11 +678,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     // =========================== epilogue (2 warpgroups)
     const int ew = warp - 8, wg = ew >> 2, q = warp & 3;
     const int l = q * 32 + lane;  // output channel within the tile == TMEM lane
-    uint32_t abuf = 0;
-    uint32_t acc_uses[kAccBufs] = {0, 0, 0, 0};
+    uint32_t abuf = 0, acc_ph = 0, rbuf = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
-      mbar_wait(&ctl.tfull[slot], rphase);
+      twait(&ctl.tfull[slot], rphase, pc[9], prof_on);
       const Task t = ctl.ring[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl.tempty[slot]);
@@ -446,24 +691,39 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         // ---- dynamic quantization of h for a weight-activation down block (rows of one 32-row chunk)
         if (ew == 0 && lane == 0) {
           const int need = p.grp_n1[t.gid];
+          const unsigned long long td = prof_on ? clock64() : 0ull;
           while (ld_acquire_gpu(p.p1_done + t.gid) < need) __nanosleep(64);
+          if (prof_on) pc[14] += clock64() - td;
         }
         named_bar_sync(1, 256);
+        // per-token W-A down: the row max |h| was accumulated by the phase-0 epilogues (atomicMax);
+        // one vectorized pass quantizes the row (r = fl32(qmax/amax), s = fl32(amax/qmax), DESIGN R9)
         const LinDesc& L = E.blk[2];
         const int K = E.inter;
-        const int g = L.a_group == -1 ? K : L.a_group;
-        const int qmax = (1 << (L.a_bits - 1)) - 1;
+        const float fq = (float)((1 << (L.a_bits - 1)) - 1);
         const int sub0 = t.ntile * 32;
         for (int rr = ew; rr < 32; rr += 8) {
           const int local = sub0 + rr;
           if (local >= t.rows) break;
           const int64_t row = (int64_t)t.row0 + local;
-          const uint16_t* src = p.H + row * p.f_max;
-          int8_t* dst = p.Hq + row * p.f_max;
-          for (int gi = 0; gi < K / g; ++gi) {
-            const float s = quant_group_warp<true>(src + gi * g, dst + gi * g, g, qmax, nullptr);
-            if (lane == 0) p.Hs[row * (p.f_max / 128) + gi] = s;
+          const float amax = __uint_as_float(__ldcg(p.hmax + row));
+          const float r = amax > 0.f ? __fdiv_rn(fq, amax) : 0.f;
+          const float sc = amax > 0.f ? __fdiv_rn(amax, fq) : 1.f;
+          const uint4* src = reinterpret_cast<const uint4*>(p.H + row * p.f_max);
+          uint2* dst = reinterpret_cast<uint2*>(p.Hq + row * p.f_max);
+          for (int i = lane; i < K / 8; i += 32) {
+            const uint4 v = __ldcg(src + i);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            uint32_t o[2] = {0, 0};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float x = bf16f((uint16_t)(w[e >> 1] >> (16 * (e & 1))));
+              const float qv = fminf(fmaxf(rintf(__fmul_rn(x, r)), -fq), fq);
+              o[e >> 2] |= ((uint32_t)(int)qv & 0xFFu) << (8 * (e & 3));
+            }
+            dst[i] = make_uint2(o[0], o[1]);
           }
+          if (lane == 0) p.Hs[row * (p.f_max / 128)] = sc;
         }
         named_bar_sync(1, 256);
         if (ew == 0 && lane == 0) {
@@ -480,122 +740,156 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       const int col0 = wg * half;
       const int n = t.ntile * 128 + l;
       const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
-      float acc[64];
+      float2 acc2[32];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] = 0.f;
-      const float* xs = t.phase == 0 ? p.xs[E.blk[0].in_slot] : p.Hs;
+      for (int i = 0; i < 32; ++i) acc2[i] = make_float2(0.f, 0.f);
       const int xs_stride = t.phase == 0 ? p.d / 128 : p.f_max / 128;
+      const LinDesc& Ld = E.blk[2];
+      const int dmode = !kind_is_i8(Ld.geo.kind) ? 0 : (Ld.geo.group == 128 ? 2 : 1);
+      const int dqmax = (1 << (Ld.a_bits - 1)) - 1;
 
       for (int si = 0; si < nsl; ++si) {
-        const SubLoop& s = sl[si];
-        const int nbuf = (s.nmats == 2 && !s.g128) ? 2 : 1;
+        const SubLoop s = sl[si];
+        const bool two = s.nmats == 2;
+        const bool nbuf2 = two && !s.g128;
         const int nev = s.g128 ? s.ns : 1;
         const float* xs_s = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;
+        const uint16_t* wsc0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off);
+        const uint16_t* wsc1 =
+            two ? reinterpret_cast<const uint16_t*>(s.mat[1]->packed + s.mat[1]->geo.wa_scale_off) : wsc0;
+        const int64_t wN = s.mat[0]->geo.N;
+        // per-group scales of event ev (weight s_w[n, g] per thread, activation s_a[row, g] per lane-column),
+        // prefetched one event ahead so their load latency overlaps the previous drain / the MMA wait
+        const int cl = col0 + lane, ch = col0 + 32 + lane;
+        const bool vlo = lane < half && cl < t.rows, vhi = 32 + lane < half && ch < t.rows;
+        const float* xs_lo = xs_s + ((int64_t)t.row0 + cl) * xs_stride;
+        const float* xs_hi = xs_s + ((int64_t)t.row0 + ch) * xs_stride;
+        // phase 0 reads x-scales written before this kernel (read-only path, prefetched before the wait);
+        // phase 2 reads h-scales written by this kernel: only after the first accumulator wait (the MMA has
+        // then consumed Hq, so the producer's dependency wait has passed) and through L2 (ld.cg)
+        const bool pre = t.phase == 0;
+        float nsw0 = 1.f, nsw1 = 1.f, nsa_lo = 1.f, nsa_hi = 1.f;
+        if (s.i8 && pre) {
+          nsw0 = bf16f(__ldg(wsc0 + n));
+          if (two) nsw1 = bf16f(__ldg(wsc1 + n));
+          nsa_lo = vlo ? __ldg(xs_lo) : 0.f;
+          nsa_hi = vhi ? __ldg(xs_hi) : 0.f;
+        }
         for (int ev = 0; ev < nev; ++ev) {
-          uint32_t bufs[2] = {0, 0};
-          for (int b = 0; b < nbuf; ++b) {
-            bufs[b] = abuf;
-            abuf = (abuf + 1) % kAccBufs;
+          float sw0 = nsw0, sw1 = nsw1, sa_lo = nsa_lo, sa_hi = nsa_hi;
+          const uint32_t b0 = abuf;
+          abuf = (abuf + 1) & (kAccBufs - 1);
+          uint32_t b1 = b0;
+          if (nbuf2) {
+            b1 = abuf;
+            abuf = (abuf + 1) & (kAccBufs - 1);
           }
-          for (int b = 0; b < nbuf; ++b) {
-            mbar_wait(&ctl.accf[bufs[b]], acc_uses[bufs[b]] & 1);
-            ++acc_uses[bufs[b]];
+          twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
+          acc_ph ^= 1u << b0;
+          if (nbuf2) {
+            twait(&ctl.accf[b1], (acc_ph >> b1) & 1, pc[10], prof_on);
+            acc_ph ^= 1u << b1;
           }
           tc_fence_after();
-          // per-mat weight scale (weight-activation) for this event's group
-          float sw[2] = {1.f, 1.f};
-          if (s.i8) {
-            const int gi = s.g128 ? ev : 0;
-            for (int m = 0; m < s.nmats; ++m) {
-              const LinDesc& L = *s.mat[m];
-              sw[m] = bf16f(reinterpret_cast<const uint16_t*>(L.packed + L.geo.wa_scale_off)[(int64_t)gi * L.geo.N + n]);
-            }
+          if (s.i8 && !pre) {
+            sw0 = bf16f(__ldg(wsc0 + (int64_t)ev * wN + n));
+            if (two) sw1 = bf16f(__ldg(wsc1 + (int64_t)ev * wN + n));
+            sa_lo = vlo ? __ldcg(xs_lo + ev) : 0.f;
+            sa_hi = vhi ? __ldcg(xs_hi + ev) : 0.f;
           }
-          const int gi = s.g128 ? ev : 0;
+          if (s.i8 && pre && ev + 1 < nev) {
+            nsw0 = bf16f(__ldg(wsc0 + (int64_t)(ev + 1) * wN + n));
+            if (two) nsw1 = bf16f(__ldg(wsc1 + (int64_t)(ev + 1) * wN + n));
+            nsa_lo = vlo ? __ldg(xs_lo + ev + 1) : 0.f;
+            nsa_hi = vhi ? __ldg(xs_hi + ev + 1) : 0.f;
+          }
+          const uint32_t colA = b0 * 128u;
+          const uint32_t colB = nbuf2 ? b1 * 128u : b0 * 128u + 64u;
           if (!reg_mode) {
             // ---- streaming epilogue: one drain event for the whole task
+            float rw_lo = 0.f, rw_hi = 0.f;
+            if (t.phase == 2) {
+              const int cl = col0 + lane, ch = col0 + 32 + lane;
+              rw_lo = (lane < half && cl < t.rows) ? __ldg(p.row_w + t.row0 + cl) : 0.f;
+              rw_hi = (32 + lane < half && ch < t.rows) ? __ldg(p.row_w + t.row0 + ch) : 0.f;
+            }
 #pragma unroll 1
             for (int c = 0; c < half; c += 8) {
               uint32_t va[8], vb[8];
               const uint32_t cbase = (uint32_t)(col0 + c);
-              const uint32_t colA = nbuf == 2 ? bufs[0] * 128u : bufs[0] * 128u;
               tmem_ld8(lane_addr + colA + cbase, va);
-              if (s.nmats == 2) tmem_ld8(lane_addr + bufs[1] * 128u + cbase, vb);
+              if (two) tmem_ld8(lane_addr + colB + cbase, vb);
               tmem_ld_wait();
+              if (t.phase == 0) {
+                float h[8];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int col = col0 + c + j;
-                if (col >= t.rows) break;
-                const int64_t row = (int64_t)t.row0 + col;
-                float sa = 1.f;
-                if (s.i8) sa = __ldg(xs_s + row * xs_stride + gi);
-                if (t.phase == 0) {
+                for (int j = 0; j < 8; ++j) {
+                  const float sa = colval(sa_lo, sa_hi, c + j);
                   float g, u;
                   if (s.i8) {
-                    g = (float)(int32_t)va[j] * (sw[0] * sa);
-                    u = (float)(int32_t)vb[j] * (sw[1] * sa);
+                    g = (float)(int32_t)va[j] * (sw0 * sa);
+                    u = (float)(int32_t)vb[j] * (sw1 * sa);
                   } else {
                     g = __uint_as_float(va[j]);
                     u = __uint_as_float(vb[j]);
                   }
-                  p.H[row * p.f_max + n] = f2bf(silu_f(g) * u);
-                } else {
-                  float o = s.i8 ? (float)(int32_t)va[j] * (sw[0] * sa) : __uint_as_float(va[j]);
-                  o *= __ldg(p.row_w + row);
-                  p.O[row * p.d + n] = f2bf(o);
+                  h[j] = silu_f(g) * u;
+                }
+                emit_h8(p, t, dmode, dqmax, n, col0 + c, h, ctl, wg, q, lane, rbuf);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const int col = col0 + c + j;
+                  const float sa = colval(sa_lo, sa_hi, c + j);
+                  const float rw = colval(rw_lo, rw_hi, c + j);
+                  if (col < t.rows) {
+                    const int64_t row = (int64_t)t.row0 + col;
+                    const float o = s.i8 ? (float)(int32_t)va[j] * (sw0 * sa) : __uint_as_float(va[j]);
+                    p.O[row * p.d + n] = f2bf(o * rw);
+                  }
                 }
               }
             }
           } else {
             // ---- register-accumulating epilogue (g128 drains / hetero gate-up)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              if (c * 8 < half) {
-#pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                  if (m < s.nmats) {
-                    uint32_t v[8];
-                    const uint32_t colm = nbuf == 2 ? bufs[m] * 128u : bufs[0] * 128u + (uint32_t)m * 64u;
-                    tmem_ld8(lane_addr + colm + (uint32_t)(col0 + c * 8), v);
-                    tmem_ld_wait();
-                    // destination: dual (phase 0): gate -> acc[0..31], up -> acc[32..63]; single: acc[0..63]
-                    const int slot_m = (t.phase == 0) ? ((nsl == 2 ? si : m) * 32) : 0;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                      const int col = col0 + c * 8 + j;
-                      float val;
-                      if (s.i8) {
-                        const float sa = col < t.rows ? __ldg(xs_s + ((int64_t)t.row0 + col) * xs_stride + gi) : 0.f;
-                        val = (float)(int32_t)v[j] * (sw[m] * sa);
-                      } else {
-                        val = __uint_as_float(v[j]);
-                      }
-                      const int ai = slot_m + c * 8 + j;
-                      if (ai < 64) acc[ai] += val;
-                    }
-                  }
-                }
-              }
-            }
+            const bool dst_hi = t.phase == 0 && nsl == 2 && si == 1;  // hetero: the up sub-loop
+            const uint32_t aA = lane_addr + colA + (uint32_t)col0, aB = lane_addr + colB + (uint32_t)col0;
+            if (dst_hi)
+              drain_event_any<16>(half, acc2, aA, aB, s.i8, false, sw0, sw1, sa_lo, sa_hi);
+            else
+              drain_event_any<0>(half, acc2, aA, aB, s.i8, two, sw0, sw1, sa_lo, sa_hi);
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0)
-            for (int b = 0; b < nbuf; ++b) mbar_arrive(&ctl.acce[bufs[b]]);
+          if (lane == 0) {
+            mbar_arrive(&ctl.acce[b0]);
+            if (nbuf2) mbar_arrive(&ctl.acce[b1]);
+          }
         }
       }
       if (reg_mode) {
+        const float* acc = reinterpret_cast<const float*>(acc2);
+        if (t.phase == 0) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          if (c < half) {
-            const int col = col0 + c;
-            if (col < t.rows) {
-              const int64_t row = (int64_t)t.row0 + col;
-              if (t.phase == 0) {
-                if (c < 32) p.H[row * p.f_max + n] = f2bf(silu_f(acc[c]) * acc[32 + c]);
-              } else {
-                p.O[row * p.d + n] = f2bf(acc[c] * __ldg(p.row_w + row));
-              }
+          for (int cc = 0; cc < 4; ++cc) {
+            if (cc * 8 < half) {
+              float h[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) h[j] = silu_f(acc[cc * 8 + j]) * acc[32 + cc * 8 + j];
+              emit_h8(p, t, dmode, dqmax, n, col0 + cc * 8, h, ctl, wg, q, lane, rbuf);
+            }
+          }
+        } else {
+          float rw_lo = 0.f, rw_hi = 0.f;
+          const int cl = col0 + lane, ch = col0 + 32 + lane;
+          rw_lo = (lane < half && cl < t.rows) ? __ldg(p.row_w + t.row0 + cl) : 0.f;
+          rw_hi = (32 + lane < half && ch < t.rows) ? __ldg(p.row_w + t.row0 + ch) : 0.f;
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            if (c < half) {
+              const int col = col0 + c;
+              const float rw = colval(rw_lo, rw_hi, c);
+              if (col < t.rows) p.O[((int64_t)t.row0 + col) * p.d + n] = f2bf(acc[c] * rw);
             }
           }
         }
@@ -610,8 +904,15 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       if (ew == 0 && lane == 0) atomicAdd(p.meta + 6, 1);
     }
   }
+  if (prof_on && lane == 0 && (warp == 0 || warp == 1 || warp == 4 || warp == 8)) {
+    // one representative thread per role: producer (0-2), MMA (3-6, 13), transform (7-8), epilogue (9-10, 14)
+    unsigned long long* dst = p.prof + (size_t)blockIdx.x * 16;
+    for (int i = 0; i < 15; ++i)
+      if (pc[i]) atomicAdd(dst + i, pc[i]);
+    if (warp == 0) atomicAdd(dst + 15, clock64() - t_start);
+  }
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }

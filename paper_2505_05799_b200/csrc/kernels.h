@@ -21,9 +21,11 @@ struct GemmParams {
   uint16_t* H;
   int8_t* Hq;
   float* Hs;
+  uint32_t* hmax;  // per route row: max |h| (fp32 bits) for per-token W-A downs (order-independent atomicMax)
   uint16_t* O;
   const float* row_w;
   int d, f_max;
+  unsigned long long* prof;  // optional [grid][16] cycle counters per wait site (nullptr = off)
 };
 
 cudaError_t launch_quantize(const PackGeom& g, const void* w, void* codes, void* scale, void* zero, int32_t* err,
@@ -41,7 +43,7 @@ cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T
                               void* scratch, cudaStream_t st);
 cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, const int32_t* row_exp,
                                 const int32_t* v_off, int V, const ExpertDesc* ex, int64_t R, void* Xb, void* XqA,
-                                float* XsA, void* XqB, float* XsB, cudaStream_t st);
+                                float* XsA, void* XqB, float* XsB, uint32_t* hmax, cudaStream_t st);
 cudaError_t launch_combine(const void* O, int d, int64_t T, int k, int S, const int32_t* inv, void* y,
                            cudaStream_t st);
 cudaError_t launch_plan(const ExpertDesc* ex, int V, int E, int64_t T, int d, const int32_t* v_off, int g_max,

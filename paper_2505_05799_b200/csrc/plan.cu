@@ -17,6 +17,34 @@ namespace mxm {
 constexpr int kPlanThreads = 1024;
 constexpr int kMaxV = 256;
 
+// exclusive block-wide scan of one int per thread (kPlanThreads threads); returns the block total
+__device__ int block_excl_scan(int v, int* warp_tot, int* out_total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  const int base = w > 0 ? warp_tot[w - 1] : 0;
+  const int total = warp_tot[31];
+  __syncthreads();
+  *out_total = total;
+  return base + x - v;
+}
+
 __device__ __forceinline__ int pow2_tile(int m) {
   return m <= 16 ? 16 : (m <= 32 ? 32 : (m <= 64 ? 64 : 128));
 }
@@ -37,11 +65,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
                                                             int32_t* __restrict__ meta, int32_t* __restrict__ grp_n1,
                                                             int32_t* __restrict__ grp_nq, int32_t* __restrict__ p1_done,
                                                             int32_t* __restrict__ hq_done) {
-  __shared__ int s_cnt[kMaxV], s_cap[kMaxV], s_nfull[kMaxV], s_rem[kMaxV], s_base[kMaxV], s_ragid[kMaxV];
+  __shared__ int s_cap[kMaxV], s_nfull[kMaxV], s_rem[kMaxV], s_base[kMaxV], s_ragid[kMaxV];
   __shared__ float s_cf[kMaxV], s_cr[kMaxV];
   __shared__ int s_order[kMaxV];
   __shared__ int s_G, s_full;
-  __shared__ int64_t s_part[3][kPlanThreads];
   const int tid = threadIdx.x;
   if (tid < V) {
     const ExpertDesc& e = ex[tid];
@@ -50,7 +77,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
       cnt = ((tid + 1 < E) ? v_off[tid + 1] : v_off[V]) - v_off[tid];
     else
       cnt = (int)T;
-    const bool reg_dual = !e.same_gu || (kind_is_i8(e.blk[0].geo.kind) && e.blk[0].geo.group == 128);
+    const bool reg_dual = !e.dual || (kind_is_i8(e.blk[0].geo.kind) && e.blk[0].geo.group == 128);
     const int cap = reg_dual ? 64 : 128;
     int nfull = 0, rem = 0;
     if (cnt > cap) {
@@ -59,7 +86,6 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
     } else {
       rem = cnt;
     }
-    s_cnt[tid] = cnt;
     s_cap[tid] = cap;
     s_nfull[tid] = nfull;
     s_rem[tid] = rem;
@@ -67,41 +93,39 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
     s_cr[tid] = rem > 0 ? tile_cost(e, d, pow2_tile(rem)) : 0.f;
   }
   __syncthreads();
+  // LPT order (parallel rank sort, V <= 256): experts with full tiles by full-tile cost desc (ties: lower
+  // id) form the first groups; then every ragged / small group ordered by its own cost desc
+  if (tid < V) {
+    const int v = tid;
+    int rf = 0, rr = 0;
+    for (int u = 0; u < V; ++u) {
+      if (s_nfull[u] > 0 && (s_cf[u] > s_cf[v] || (s_cf[u] == s_cf[v] && u < v))) ++rf;
+      if (s_rem[u] > 0 && (s_cr[u] > s_cr[v] || (s_cr[u] == s_cr[v] && u < v))) ++rr;
+    }
+    s_order[v] = (s_nfull[v] > 0) ? rf : -1;  // rank among experts with full tiles
+    s_ragid[v] = (s_rem[v] > 0) ? rr : -1;    // rank among ragged groups
+  }
+  __syncthreads();
   if (tid == 0) {
-    // LPT order: experts with full tiles by full-tile cost desc (ties: lower id), then ragged groups
-    int n = 0;
-    for (int v = 0; v < V; ++v)
-      if (s_nfull[v] > 0) s_order[n++] = v;
-    for (int i = 1; i < n; ++i) {  // insertion sort, V <= 256
-      const int v = s_order[i];
-      int j = i - 1;
-      while (j >= 0 && (s_cf[s_order[j]] < s_cf[v] || (s_cf[s_order[j]] == s_cf[v] && s_order[j] > v))) {
-        s_order[j + 1] = s_order[j];
-        --j;
+    int rank_to_v[kMaxV];
+    int nf = 0, nr = 0;
+    for (int v = 0; v < V; ++v) {
+      if (s_order[v] >= 0) {
+        rank_to_v[s_order[v]] = v;
+        ++nf;
       }
-      s_order[j + 1] = v;
+      if (s_ragid[v] >= 0) ++nr;
     }
     int base = 0;
-    for (int i = 0; i < n; ++i) {
-      s_base[s_order[i]] = base;
-      base += s_nfull[s_order[i]];
+    for (int i = 0; i < nf; ++i) {
+      s_base[rank_to_v[i]] = base;
+      base += s_nfull[rank_to_v[i]];
     }
     s_full = base;
-    n = 0;
-    for (int v = 0; v < V; ++v)
-      if (s_rem[v] > 0) s_order[n++] = v;
-    for (int i = 1; i < n; ++i) {
-      const int v = s_order[i];
-      int j = i - 1;
-      while (j >= 0 && (s_cr[s_order[j]] < s_cr[v] || (s_cr[s_order[j]] == s_cr[v] && s_order[j] > v))) {
-        s_order[j + 1] = s_order[j];
-        --j;
-      }
-      s_order[j + 1] = v;
-    }
-    for (int i = 0; i < n; ++i) s_ragid[s_order[i]] = base + i;
-    s_G = base + n;
+    s_G = base + nr;
   }
+  __syncthreads();
+  if (tid < V && s_ragid[tid] >= 0) s_ragid[tid] += s_full;
   __syncthreads();
   const int G = s_G;
   if (G > g_max) {
@@ -116,7 +140,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
   if (tid < V) {
     const int v = tid;
     const ExpertDesc& e = ex[v];
-    const bool wa_down = kind_is_i8(e.blk[2].geo.kind);
+    // h-quant pass only for per-token W-A downs (g128 downs are quantized in the gate/up epilogue)
+    const bool wa_down = kind_is_i8(e.blk[2].geo.kind) && e.blk[2].geo.group != 128;
     for (int i = 0; i < s_nfull[v]; ++i) {
       const int g = s_base[v] + i;
       grp_v[g] = v;
@@ -144,39 +169,29 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
   // prefix sums of per-group task counts (3 phases); each thread owns a contiguous gid range
   const int per = (G + kPlanThreads - 1) / kPlanThreads;
   const int g0 = min(G, tid * per), g1 = min(G, g0 + per);
-  int64_t c1 = 0, cq = 0, c2 = 0;
+  int c1 = 0, cq = 0, c2 = 0;
   for (int g = g0; g < g1; ++g) {
     c1 += grp_n1[g];
     cq += grp_nq[g];
     c2 += d / 128;
   }
-  s_part[0][tid] = c1;
-  s_part[1][tid] = cq;
-  s_part[2][tid] = c2;
-  __syncthreads();
+  __shared__ int s_wt[32];
+  int t1, tq, t2;
+  const int e1 = block_excl_scan(c1, s_wt, &t1);
+  const int eq = block_excl_scan(cq, s_wt, &tq);
+  const int e2 = block_excl_scan(c2, s_wt, &t2);
+  const int64_t total = (int64_t)t1 + tq + t2;
   if (tid == 0) {
-    int64_t r[3] = {0, 0, 0};
-    for (int i = 0; i < kPlanThreads; ++i)
-      for (int p = 0; p < 3; ++p) {
-        const int64_t v = s_part[p][i];
-        s_part[p][i] = r[p];
-        r[p] += v;
-      }
-    const int64_t total = r[0] + r[1] + r[2];
     meta[0] = total <= task_cap ? (int32_t)total : -1;
-    meta[1] = (int32_t)r[0];
-    meta[2] = (int32_t)r[1];
-    meta[3] = (int32_t)r[2];
+    meta[1] = t1;
+    meta[2] = tq;
+    meta[3] = t2;
     meta[4] = G;
     meta[5] = 0;  // queue head
     meta[6] = 0;  // executed-task counter (debug)
-    s_part[1][kPlanThreads - 1] += 0;
-    s_G = (int)r[0];
-    s_full = (int)(r[0] + r[1]);
   }
-  __syncthreads();
-  if (meta[0] < 0) return;
-  int64_t o1 = s_part[0][tid], oq = (int64_t)s_G + s_part[1][tid], o2 = (int64_t)s_full + s_part[2][tid];
+  if (total > task_cap) return;
+  int64_t o1 = e1, oq = (int64_t)t1 + eq, o2 = (int64_t)t1 + tq + e2;
   for (int g = g0; g < g1; ++g) {
     Task t;
     t.expert = (uint16_t)grp_v[g];

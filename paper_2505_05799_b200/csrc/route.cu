@@ -133,17 +133,18 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
                                     const int32_t* __restrict__ row_exp, const int32_t* __restrict__ v_off, int V,
                                     const ExpertDesc* __restrict__ ex,
                                     int64_t R, uint16_t* __restrict__ Xb, int8_t* __restrict__ XqA, float* __restrict__ XsA,
-                                    int8_t* __restrict__ XqB, float* __restrict__ XsB) {
+                                    int8_t* __restrict__ XqB, float* __restrict__ XsB, uint32_t* __restrict__ hmax) {
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (row >= R) return;
   if (row >= v_off[V]) return;  // rows past the last valid route are unused
   const int v = row_exp[row];
+  if (lane == 0 && hmax) hmax[row] = 0u;
   const ExpertDesc& E = ex[v];
   const uint16_t* src = x + (int64_t)row_src[row] * d;
   for (int b = 0; b < 2; ++b) {
     const LinDesc& L = E.blk[b];
-    if (b == 1 && E.same_gu) break;
+    if (b == 1 && E.blk[1].in_slot == E.blk[0].in_slot) break;
     if (L.in_slot == 0) {
       const uint4* s4 = reinterpret_cast<const uint4*>(src);
       uint4* d4 = reinterpret_cast<uint4*>(Xb + row * d);
@@ -228,10 +229,10 @@ cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T
 cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, const int32_t* row_exp,
                                 const int32_t* v_off, int V,
                                 const ExpertDesc* ex, int64_t R, void* Xb, void* XqA, float* XsA, void* XqB, float* XsB,
-                                cudaStream_t st) {
+                                uint32_t* hmax, cudaStream_t st) {
   if (R <= 0) return cudaSuccess;
   gather_quant_kernel<<<(unsigned)((R * 32 + 255) / 256), 256, 0, st>>>(
-      (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB);
+      (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB, hmax);
   return cudaGetLastError();
 }
 
