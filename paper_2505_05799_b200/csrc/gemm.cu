@@ -27,18 +27,16 @@
 
 namespace mxm {
 
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kRing = 4;
-constexpr int kAccBufs = 4;
+constexpr int kAccBufs = 2;      // accumulator buffers of 128 TMEM columns at [0, 256)
+constexpr int kTmemA = 256;      // TMEM A ring (dequantized weights, TS-form MMA): 4 stages x 2 mats x 32 columns
 constexpr int kThreads = 512;  // 16 warps: producer, 2 MMA issuers, idle, 4 transform, 8 epilogue
-constexpr int kXfWarps = 4;     // transform warps 4..7 (one A row per thread)
-constexpr int kRawBytes = 10752;
+constexpr int kXfWarps = 4;     // transform warps 4..7 (one A row = one TMEM lane per thread)
 constexpr int kTileBytes = 16384;
+constexpr int kSlotBytes = 3 * kTileBytes;  // per stage: token tile B | mat 0 (raw codes or A image) | mat 1
 
-constexpr int kOffA = 0;
-constexpr int kOffB = kOffA + kStages * 2 * kTileBytes;
-constexpr int kOffRaw = kOffB + kStages * kTileBytes;
-constexpr int kOffCtl = kOffRaw + kStages * 2 * kRawBytes;
+constexpr int kOffCtl = kStages * kSlotBytes;
 constexpr int kCtlBytes = 1024;
 constexpr int kSmemBytes = kOffCtl + kCtlBytes + 1024;
 
@@ -104,11 +102,12 @@ __device__ __forceinline__ uint32_t deq_pair(uint32_t fields, uint32_t off2, uin
   return bf2_fma(bf2_sub(fields | 0x43004300u, off2), s2, z2);
 }
 
-// Weight-only dequant of one A row (thread r = row r): packed codes -> bf16 q*s + z, swizzled store.
+// Weight-only dequant of one A row (thread r = TMEM lane r): packed codes -> 64 bf16 = 32 words o[] in K order
+// (o[j] = elements 2j, 2j+1), later written to the TMEM A ring with one tcgen05.st.
 // `hm`: this stage starts a group, so the chunk begins with scale[128] (and zero[128] if asymmetric).
 template <int BITS>
-__device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_t* __restrict__ A, bool hm,
-                                         int meta_bytes, bool sym, uint32_t off2, int r, uint32_t& s2, uint32_t& z2) {
+__device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, bool hm, int meta_bytes, bool sym,
+                                         uint32_t off2, int r, uint32_t& s2, uint32_t& z2, uint32_t (&o)[32]) {
   const uint8_t* codes = raw;
   if (hm) {
     const uint32_t sb = reinterpret_cast<const uint16_t*>(raw)[r];
@@ -122,34 +121,19 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_
     codes += meta_bytes;
   }
   const uint32_t* w = reinterpret_cast<const uint32_t*>(codes);
-  uint8_t* dst = A + r * 128;
-  const int sw = r & 7;
   if constexpr (BITS == 4) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t word = w[j * 128 + r];
-      uint4 o;
-      o.x = deq_pair(word & 0x000F000Fu, off2, s2, z2);
-      o.y = deq_pair((word >> 4) & 0x000F000Fu, off2, s2, z2);
-      o.z = deq_pair((word >> 8) & 0x000F000Fu, off2, s2, z2);
-      o.w = deq_pair((word >> 12) & 0x000F000Fu, off2, s2, z2);
-      *reinterpret_cast<uint4*>(dst + ((j ^ sw) << 4)) = o;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) o[4 * j + t] = deq_pair((word >> (4 * t)) & 0x000F000Fu, off2, s2, z2);
     }
   } else if constexpr (BITS == 2) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t word = w[j * 128 + r];
-      uint4 o0, o1;
-      o0.x = deq_pair(word & 0x00030003u, off2, s2, z2);
-      o0.y = deq_pair((word >> 2) & 0x00030003u, off2, s2, z2);
-      o0.z = deq_pair((word >> 4) & 0x00030003u, off2, s2, z2);
-      o0.w = deq_pair((word >> 6) & 0x00030003u, off2, s2, z2);
-      o1.x = deq_pair((word >> 8) & 0x00030003u, off2, s2, z2);
-      o1.y = deq_pair((word >> 10) & 0x00030003u, off2, s2, z2);
-      o1.z = deq_pair((word >> 12) & 0x00030003u, off2, s2, z2);
-      o1.w = deq_pair((word >> 14) & 0x00030003u, off2, s2, z2);
-      *reinterpret_cast<uint4*>(dst + (((2 * j) ^ sw) << 4)) = o0;
-      *reinterpret_cast<uint4*>(dst + (((2 * j + 1) ^ sw) << 4)) = o1;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) o[8 * j + t] = deq_pair((word >> (2 * t)) & 0x00030003u, off2, s2, z2);
     }
   } else if constexpr (BITS == 3) {
     const uint32_t* wh = w + 4 * 128;
@@ -158,88 +142,65 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, uint8_
     for (int j = 0; j < 4; ++j) {
       const uint32_t word = w[j * 128 + r];
       const uint32_t hw = ((j >> 1) ? h1 : h0) >> (8 * (j & 1));
-      uint32_t p[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t)
-        p[t] = deq_pair(((word >> (2 * t)) & 0x00030003u) | (((hw >> t) & 0x00010001u) << 2), off2, s2, z2);
-      *reinterpret_cast<uint4*>(dst + (((2 * j) ^ sw) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
-      *reinterpret_cast<uint4*>(dst + (((2 * j + 1) ^ sw) << 4)) = make_uint4(p[4], p[5], p[6], p[7]);
+        o[8 * j + t] = deq_pair(((word >> (2 * t)) & 0x00030003u) | (((hw >> t) & 0x00010001u) << 2), off2, s2, z2);
     }
   } else {  // 8-bit: fp32 path (128 + u is not exact in bf16 for u >= 128)
     const float sf = __uint_as_float(s2 << 16), zf = __uint_as_float(z2 << 16);
-    const float fo = (float)((off2 & 0xFFu));
+    const float fo = (float)(off2 & 0xFFu);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      uint32_t o[4];
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = w[j * 128 + r];
+      float f[4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t word = w[(2 * c + h) * 128 + r];
-        float f[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) f[b] = (__uint_as_float(0x4B000000u | ((word >> (8 * b)) & 0xFFu)) - 8388608.f) - fo;
-        __nv_bfloat162 lo = __floats2bfloat162_rn(fmaf(f[0], sf, zf), fmaf(f[1], sf, zf));
-        __nv_bfloat162 hi = __floats2bfloat162_rn(fmaf(f[2], sf, zf), fmaf(f[3], sf, zf));
-        o[2 * h] = *reinterpret_cast<uint32_t*>(&lo);
-        o[2 * h + 1] = *reinterpret_cast<uint32_t*>(&hi);
-      }
-      *reinterpret_cast<uint4*>(dst + ((c ^ sw) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+      for (int b = 0; b < 4; ++b) f[b] = (__uint_as_float(0x4B000000u | ((word >> (8 * b)) & 0xFFu)) - 8388608.f) - fo;
+      __nv_bfloat162 lo = __floats2bfloat162_rn(fmaf(f[0], sf, zf), fmaf(f[1], sf, zf));
+      __nv_bfloat162 hi = __floats2bfloat162_rn(fmaf(f[2], sf, zf), fmaf(f[3], sf, zf));
+      o[2 * j] = *reinterpret_cast<uint32_t*>(&lo);
+      o[2 * j + 1] = *reinterpret_cast<uint32_t*>(&hi);
     }
   }
 }
 
-__device__ __forceinline__ void xform_wo_any(int bits, const uint8_t* raw, uint8_t* A, bool hm, int mb, bool sym,
-                                             uint32_t off2, int r, uint32_t& s2, uint32_t& z2) {
+__device__ __forceinline__ void xform_wo_any(int bits, const uint8_t* raw, bool hm, int mb, bool sym, uint32_t off2,
+                                             int r, uint32_t& s2, uint32_t& z2, uint32_t (&o)[32]) {
   switch (bits) {
     case 2:
-      xform_wo<2>(raw, A, hm, mb, sym, off2, r, s2, z2);
+      xform_wo<2>(raw, hm, mb, sym, off2, r, s2, z2, o);
       break;
     case 3:
-      xform_wo<3>(raw, A, hm, mb, sym, off2, r, s2, z2);
+      xform_wo<3>(raw, hm, mb, sym, off2, r, s2, z2, o);
       break;
     case 4:
-      xform_wo<4>(raw, A, hm, mb, sym, off2, r, s2, z2);
+      xform_wo<4>(raw, hm, mb, sym, off2, r, s2, z2, o);
       break;
     default:
-      xform_wo<8>(raw, A, hm, mb, sym, off2, r, s2, z2);
+      xform_wo<8>(raw, hm, mb, sym, off2, r, s2, z2, o);
       break;
   }
 }
 
 __device__ __forceinline__ uint32_t to_s8_4(uint32_t u, uint32_t bias) { return (u + bias) ^ 0x80808080u; }
 
+// W-A w4/w5 unpack of one row: 128 codes -> s8, o[j] = bytes 4j..4j+3 in K order
 template <int BITS>
-__device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, uint8_t* __restrict__ A, int r) {
+__device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, int r, uint32_t (&o)[32]) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(raw);
-  uint8_t* dst = A + r * 128;
-  const int sw = r & 7;
-  if constexpr (BITS == 4) {
+  const uint32_t* wh = w + 16 * 128;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t w0 = w[(2 * c) * 128 + r], w1 = w[(2 * c + 1) * 128 + r];
-      uint4 o;
-      o.x = to_s8_4(w0 & 0x0F0F0F0Fu, 0x78787878u);
-      o.y = to_s8_4((w0 >> 4) & 0x0F0F0F0Fu, 0x78787878u);
-      o.z = to_s8_4(w1 & 0x0F0F0F0Fu, 0x78787878u);
-      o.w = to_s8_4((w1 >> 4) & 0x0F0F0F0Fu, 0x78787878u);
-      *reinterpret_cast<uint4*>(dst + ((c ^ sw) << 4)) = o;
-    }
-  } else {  // w5: 4-bit plane (16 words) + 1-bit plane (4 words)
-    const uint32_t* wh = w + 16 * 128;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      uint32_t o[4];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = 2 * c + h;
-        const uint32_t word = w[j * 128 + r];
-        const uint32_t hb = wh[(j >> 2) * 128 + r];
-        const int t0 = 2 * (j & 3);
-        const uint32_t lo = (word & 0x0F0F0F0Fu) | (((hb >> t0) & 0x01010101u) << 4);
-        const uint32_t hi = ((word >> 4) & 0x0F0F0F0Fu) | (((hb >> (t0 + 1)) & 0x01010101u) << 4);
-        o[2 * h] = to_s8_4(lo, 0x70707070u);
-        o[2 * h + 1] = to_s8_4(hi, 0x70707070u);
-      }
-      *reinterpret_cast<uint4*>(dst + ((c ^ sw) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t word = w[j * 128 + r];
+    if constexpr (BITS == 4) {
+      o[2 * j] = to_s8_4(word & 0x0F0F0F0Fu, 0x78787878u);
+      o[2 * j + 1] = to_s8_4((word >> 4) & 0x0F0F0F0Fu, 0x78787878u);
+    } else {
+      const uint32_t hb = wh[(j >> 2) * 128 + r];
+      const int t0 = 2 * (j & 3);
+      const uint32_t lo = (word & 0x0F0F0F0Fu) | (((hb >> t0) & 0x01010101u) << 4);
+      const uint32_t hi = ((word >> 4) & 0x0F0F0F0Fu) | (((hb >> (t0 + 1)) & 0x01010101u) << 4);
+      o[2 * j] = to_s8_4(lo, 0x70707070u);
+      o[2 * j + 1] = to_s8_4(hi, 0x70707070u);
     }
   }
 }
@@ -404,15 +365,24 @@ struct MmaState {
 
 // One sub-loop of MMAs (all K stages of one or two mats sharing the token tile), specialised on the MMA
 // kind and the number of mats so the issue loop has no runtime kind branches.
-template <bool I8, bool TWO, int ROLE>
-__device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tmem, const SubLoop& s, uint32_t nt,
-                                            MmaState& st, unsigned long long (&pc)[16], bool prof_on) {
-  const bool nbuf2 = TWO && !s.g128;
+__device__ __forceinline__ uint32_t bcast(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+
+// One sub-loop of MMAs (all K stages of one or two mats sharing the token tile), specialised on the MMA
+// kind and the number of mats. Executed by the whole MMA warp with warp-uniform operands (broadcast from
+// lane 0) and the tcgen05 instructions inside one elect.sync block per stage: this keeps the operands in
+// uniform registers (no per-lane "waterfall" loop around each MMA) — the issue queue is shallow, so every
+// instruction between MMAs costs tensor-core time.
+template <bool I8, bool TWO>
+__device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tmem, uint32_t ns, uint32_t g128,
+                                            uint32_t xform, uint32_t nt, MmaState& st, unsigned long long (&pc)[16],
+                                            bool prof_on) {
+  const bool nbuf2 = TWO && !g128;
   const uint32_t idesc = I8 ? idesc_s8(nt) : idesc_bf16(nt);
-  const uint32_t a_base = smem_u32(smem + kOffA), b_base = smem_u32(smem + kOffB);
+  const uint32_t s_base = smem_u32(smem);
+  const bool ts0 = (xform & 1) != 0, ts1 = (xform & 2) != 0;  // transformed mats read A from TMEM
   uint32_t b0 = 0, b1 = 0;
-  for (int ks = 0; ks < s.ns; ++ks) {
-    const bool ev_start = s.g128 || ks == 0, ev_end = s.g128 || ks == s.ns - 1;
+  for (uint32_t ks = 0; ks < ns; ++ks) {
+    const bool ev_start = g128 || ks == 0, ev_end = g128 || ks == ns - 1;
     if (ev_start) {
       b0 = st.abuf;
       twait(&ctl.acce[b0], ((st.acc_ph >> b0) & 1) ^ 1, pc[4], prof_on);
@@ -426,36 +396,48 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
       }
     }
     const uint32_t stage = st.stage;
-    twait(&ctl.full[stage], st.sphase, pc[5], prof_on);
-    if (s.xform) {
+    // one wait per stage: transformed stages complete `aready` only after the transform saw `full`
+    if (xform) {
       twait(&ctl.aready[stage], (st.ar_ph >> stage) & 1, pc[6], prof_on);
       st.ar_ph ^= 1u << stage;
+    } else {
+      twait(&ctl.full[stage], st.sphase, pc[5], prof_on);
     }
     tc_fence_after();
-    const uint32_t bb = b_base + stage * kTileBytes;
-    const uint32_t a0 = a_base + (stage * 2) * kTileBytes, a1 = a0 + kTileBytes;
+    const uint32_t bb = s_base + stage * kSlotBytes;
     const uint32_t d0 = tmem + b0 * 128u;
     const uint32_t d1 = nbuf2 ? tmem + b1 * 128u : tmem + b0 * 128u + 64u;
     const uint32_t acc0 = ev_start ? 0u : 1u;
-    // ROLE 0 (warp 1) issues mat 0 (gate / the single block); ROLE 1 (warp 2) issues mat 1 (up), so each
-    // warp's barrier / commit latency is covered by the other warp's MMAs (the tcgen05 issue queue is shallow)
-    if constexpr (ROLE == 0 || TWO) {
-      const uint32_t dd = ROLE == 0 ? d0 : d1;
-      const uint32_t aa = ROLE == 0 ? a0 : a1;
+    const uint32_t as0 = bb + kTileBytes, as1 = bb + 2 * kTileBytes;   // A images (SS form)
+    const uint32_t at0 = tmem + kTmemA + stage * 64u, at1 = at0 + 32u;  // A in TMEM (TS form)
+    const unsigned long long t_iss = prof_on ? clock64() : 0ull;
+    if (elect_one()) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t acc = k == 0 ? acc0 : 1u;
-        if constexpr (I8)
-          mma_i8(dd, sw128_kmajor_desc(aa + k * 32), sw128_kmajor_desc(bb + k * 32), idesc, acc);
-        else
-          mma_bf16(dd, sw128_kmajor_desc(aa + k * 32), sw128_kmajor_desc(bb + k * 32), idesc, acc);
+        const uint64_t bd = sw128_kmajor_desc(bb + k * 32);
+        if constexpr (I8) {
+          if (ts0) mma_i8_ts(d0, at0 + k * 8, bd, idesc, acc); else mma_i8(d0, sw128_kmajor_desc(as0 + k * 32), bd, idesc, acc);
+          if constexpr (TWO) {
+            if (ts1) mma_i8_ts(d1, at1 + k * 8, bd, idesc, acc); else mma_i8(d1, sw128_kmajor_desc(as1 + k * 32), bd, idesc, acc);
+          }
+        } else {
+          if (ts0) mma_bf16_ts(d0, at0 + k * 8, bd, idesc, acc); else mma_bf16(d0, sw128_kmajor_desc(as0 + k * 32), bd, idesc, acc);
+          if constexpr (TWO) {
+            if (ts1) mma_bf16_ts(d1, at1 + k * 8, bd, idesc, acc); else mma_bf16(d1, sw128_kmajor_desc(as1 + k * 32), bd, idesc, acc);
+          }
+        }
+      }
+      mma_commit(&ctl.empty[stage]);
+      if (ev_end) {
+        mma_commit(&ctl.accf[b0]);
+        if (nbuf2) mma_commit(&ctl.accf[b1]);
       }
     }
-    mma_commit(&ctl.empty[stage]);
-    if (prof_on) pc[13] += 1;
-    if (ev_end) {
-      mma_commit(&ctl.accf[b0]);
-      if (nbuf2) mma_commit(&ctl.accf[b1]);
+    __syncwarp();
+    if (prof_on) {
+      pc[11] += clock64() - t_iss;
+      pc[13] += 1;
     }
     if (++st.stage == kStages) {
       st.stage = 0;
@@ -467,26 +449,26 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // keep the pointer in the shared window (no uintptr_t round trip) so tile accesses compile to LDS/STS
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Ctl& ctl = *reinterpret_cast<Ctl*>(smem + kOffCtl);
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  auto tileA = [&](int s, int m) { return smem + kOffA + (s * 2 + m) * kTileBytes; };
-  auto tileB = [&](int s) { return smem + kOffB + s * kTileBytes; };
-  auto tileRaw = [&](int s, int m) { return smem + kOffRaw + (s * 2 + m) * kRawBytes; };
+  auto tileB = [&](int s) { return smem + s * kSlotBytes; };
+  auto tileX = [&](int s, int m) { return smem + s * kSlotBytes + (1 + m) * kTileBytes; };  // raw codes / A image
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&ctl.full[i], 1);
-      mbar_init(&ctl.empty[i], 2);  // both MMA warps commit every stage
+      mbar_init(&ctl.empty[i], 1);
       mbar_init(&ctl.aready[i], kXfWarps);
     }
     for (int i = 0; i < kAccBufs; ++i) {
-      mbar_init(&ctl.accf[i], 2);  // both MMA warps commit at every drain event
+      mbar_init(&ctl.accf[i], 1);
       mbar_init(&ctl.acce[i], 8);
     }
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&ctl.tfull[i], 1);
-      mbar_init(&ctl.tempty[i], 2 + kXfWarps + 8);
+      mbar_init(&ctl.tempty[i], 1 + kXfWarps + 8);
     }
     fence_mbar_init();
   }
@@ -549,10 +531,9 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const int gst0 = g0.group / g0.ks, gst1 = g1.group / g1.ks;
           const uint8_t* src0 = s.mat[0]->packed + (int64_t)t.ntile * g0.rb_bytes;
           const uint8_t* src1 = s.nmats == 2 ? s.mat[1]->packed + (int64_t)t.ntile * g1.rb_bytes : nullptr;
-          uint8_t* const dst0 = (s.xform & 1) ? tileRaw(0, 0) : tileA(0, 0);
-          uint8_t* const dst1 = (s.xform & 2) ? tileRaw(0, 1) : tileA(0, 1);
-          const int str0 = (s.xform & 1) ? 2 * kRawBytes : 2 * kTileBytes;
-          const int str1 = (s.xform & 2) ? 2 * kRawBytes : 2 * kTileBytes;
+          uint8_t* const dst0 = tileX(0, 0);
+          uint8_t* const dst1 = tileX(0, 1);
+          const int str0 = kSlotBytes, str1 = kSlotBytes;
           const int kstep = s.i8 ? 128 : 64;
           int gc0 = 0, gc1 = 0;
           for (int ks = 0; ks < s.ns; ++ks) {
@@ -578,42 +559,45 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       }
     }
     __syncwarp();
-  } else if (warp == 1 || warp == 2) {
-    // =========================== MMA issuers (warp 1: mat 0, warp 2: mat 1)
-    if (lane == 0) {
-      uint32_t stage = 0, sphase = 0, abuf = 0;
-      uint32_t acc_ph = 0;  // bit b: parity of the next wait on acce[b] (phase bits, no local arrays)
-      uint32_t ar_ph = 0;   // bit s: parity of the next wait on aready[s]
-      for (uint32_t it = 0;; ++it) {
-        const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
-        twait(&ctl.tfull[slot], rphase, pc[3], prof_on);
-        const Task t = ctl.ring[slot];
-        mbar_arrive(&ctl.tempty[slot]);
-        if (t.phase == 255) break;
-        if (t.phase == 1) continue;
-        SubLoop sl[2];
-        const int nsl = build_subloops(t, p.ex, sl);
-        for (int si = 0; si < nsl; ++si) {
-          const SubLoop s = sl[si];
-          MmaState st{stage, sphase, abuf, acc_ph, ar_ph};
-          const uint32_t nt = t.nt;
-          if (s.i8) {
-            if (s.nmats == 2)
-              (warp == 1 ? mma_subloop<true, true, 0>(ctl, smem, tmem, s, nt, st, pc, prof_on) : mma_subloop<true, true, 1>(ctl, smem, tmem, s, nt, st, pc, prof_on));
-            else
-              (warp == 1 ? mma_subloop<true, false, 0>(ctl, smem, tmem, s, nt, st, pc, prof_on) : mma_subloop<true, false, 1>(ctl, smem, tmem, s, nt, st, pc, prof_on));
-          } else {
-            if (s.nmats == 2)
-              (warp == 1 ? mma_subloop<false, true, 0>(ctl, smem, tmem, s, nt, st, pc, prof_on) : mma_subloop<false, true, 1>(ctl, smem, tmem, s, nt, st, pc, prof_on));
-            else
-              (warp == 1 ? mma_subloop<false, false, 0>(ctl, smem, tmem, s, nt, st, pc, prof_on) : mma_subloop<false, false, 1>(ctl, smem, tmem, s, nt, st, pc, prof_on));
-          }
-          stage = st.stage;
-          sphase = st.sphase;
-          abuf = st.abuf;
-          acc_ph = st.acc_ph;
-          ar_ph = st.ar_ph;
+  } else if (warp == 1) {
+    // =========================== MMA issuer (whole warp; one elected lane issues; one stream per SM)
+    const uint32_t tm = bcast(tmem);
+    uint32_t stage = 0, sphase = 0, abuf = 0;
+    uint32_t acc_ph = 0;  // bit b: parity of the next wait on acce[b] (phase bits, no local arrays)
+    uint32_t ar_ph = 0;   // bit s: parity of the next wait on aready[s]
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
+      twait(&ctl.tfull[slot], rphase, pc[3], prof_on);
+      const Task t = ctl.ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl.tempty[slot]);
+      const uint32_t phase = bcast(t.phase);
+      if (phase == 255) break;
+      if (phase == 1) continue;
+      SubLoop sl[2];
+      const int nsl = (int)bcast((uint32_t)build_subloops(t, p.ex, sl));
+      const uint32_t nt = bcast(t.nt);
+      for (int si = 0; si < nsl; ++si) {
+        const SubLoop s = sl[si];
+        const uint32_t ns = bcast((uint32_t)s.ns), g128 = bcast((uint32_t)s.g128), xf = bcast((uint32_t)s.xform);
+        const uint32_t i8 = bcast((uint32_t)s.i8), two = bcast((uint32_t)(s.nmats == 2));
+        MmaState st{stage, sphase, abuf, acc_ph, ar_ph};
+        if (i8) {
+          if (two)
+            mma_subloop<true, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+          else
+            mma_subloop<true, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+        } else {
+          if (two)
+            mma_subloop<false, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+          else
+            mma_subloop<false, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
         }
+        stage = st.stage;
+        sphase = st.sphase;
+        abuf = st.abuf;
+        acc_ph = st.acc_ph;
+        ar_ph = st.ar_ph;
       }
     }
     __syncwarp();
@@ -651,19 +635,29 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           if (++gcb == gstB) gcb = 0;
           if (s.xform) {
             twait(&ctl.full[stage], sphase, pc[8], prof_on);
+            // dequantized / unpacked rows go to the TMEM A ring (lane = row); one tcgen05.st per mat
+            const uint32_t tA = tmem + ((uint32_t)(r & ~31) << 16) + kTmemA + stage * 64u;
+            uint32_t o[32];
             if (s.i8) {
-              if (bitsA == 4) {
-                if (xa) xform_wa<4>(tileRaw(stage, 0), tileA(stage, 0), r);
-                if (xb) xform_wa<4>(tileRaw(stage, 1), tileA(stage, 1), r);
-              } else {
-                if (xa) xform_wa<5>(tileRaw(stage, 0), tileA(stage, 0), r);
-                if (xb) xform_wa<5>(tileRaw(stage, 1), tileA(stage, 1), r);
+              if (xa) {
+                if (bitsA == 4) xform_wa<4>(tileX(stage, 0), r, o); else xform_wa<5>(tileX(stage, 0), r, o);
+                tmem_st32(tA, o);
+              }
+              if (xb) {
+                if (bitsB == 4) xform_wa<4>(tileX(stage, 1), r, o); else xform_wa<5>(tileX(stage, 1), r, o);
+                tmem_st32(tA + 32, o);
               }
             } else {
-              if (xa) xform_wo_any(bitsA, tileRaw(stage, 0), tileA(stage, 0), hmA, mbA, symA, offA, r, sa, za);
-              if (xb) xform_wo_any(bitsB, tileRaw(stage, 1), tileA(stage, 1), hmB, mbB, symB, offB, r, sb, zb);
+              if (xa) {
+                xform_wo_any(bitsA, tileX(stage, 0), hmA, mbA, symA, offA, r, sa, za, o);
+                tmem_st32(tA, o);
+              }
+              if (xb) {
+                xform_wo_any(bitsB, tileX(stage, 1), hmB, mbB, symB, offB, r, sb, zb, o);
+                tmem_st32(tA + 32, o);
+              }
             }
-            fence_proxy_async_smem();
+            tmem_st_wait();
             __syncwarp();
             if (lane == 0) mbar_arrive(&ctl.aready[stage]);
           }
