@@ -10,8 +10,10 @@ combine) over one batch of T tokens whose inputs are resident in HBM; L2 is flus
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config dsv2|q15|mx|q2|tiny] [--tokens T]
   python bench.py --impl reference ...   (the CPU oracle on bounded token samples)
 
-N > 1 (torchrun, one rank per GPU): each rank runs its own batch through a full replica of the
-layer (data-parallel replicas, no data-path collective; "scaling": "weak").
+N > 1 (torchrun, one rank per GPU): expert parallelism. Rank r owns routed experts
+[r·E/G, (r+1)·E/G) and its own batch of T tokens (weak scaling: per-GPU tokens and per-GPU expert work
+fixed as N grows); tokens are dispatched to / combined from the expert owners with NCCL all-to-all
+(paper_2505_05799_b200/ep.py). `--replicas` instead runs N independent full replicas.
 """
 from __future__ import annotations
 
@@ -49,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=64, help="tokens in the cpu_baseline oracle sample")
+    ap.add_argument("--no-comparators", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent full replicas instead of EP")
     return ap.parse_args()
 
 
@@ -116,6 +120,63 @@ class ClockSampler:
         reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": float(rows[0][1]),
                 "reasons": reasons, "samples": len(rows)}
+
+
+UNIFORM_COMPARATORS = {
+    "dsv2": ["w16", "w2a16_g128_asym"],      # bf16 and the equal-bits (2.25) uniform scheme
+    "q15": ["w16", "w8a8_g-1_sym"],          # bf16 and uniform W8A8
+    "mx": ["w16", "w8a8_g-1_sym", "w4a16_g128_asym"],
+    "q2": ["w8a8_g-1_sym"],
+    "tiny": ["w16"],
+}
+
+
+def time_steps(fn, steps, flush):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record()
+        fn()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    return statistics.mean(a.elapsed_time(b) for a, b in ev)
+
+
+def bf16_grouped_block(cfg, Wt, x, ids, w, sw, steps, flush):
+    """Baseline: the bf16 MoE block with torch._grouped_mm (cuBLAS-class grouped GEMM) on the same routing.
+
+    Stand-in for the paper's CUTLASS 16-bit Group-GEMM baseline. Returns (block ms, GEMM-only ms).
+    """
+    E, S, d, f = cfg.n_routed, cfg.n_shared, cfg.hidden, cfg.inter
+    wgu = torch.stack([torch.cat([Wt[e][0], Wt[e][1]], 0).t() for e in range(E)])  # [E, d, 2f] column-major
+    wd = torch.stack([Wt[e][2].t() for e in range(E)])                            # [E, f, d]
+    T, k = ids.shape
+    flat = ids.reshape(-1).long()
+    order = torch.argsort(flat, stable=True)
+    counts = torch.bincount(flat, minlength=E)
+    offs = counts.cumsum(0).to(torch.int32)
+    tok = order // k
+    wr = w.reshape(-1)[order].unsqueeze(1).to(torch.bfloat16)
+    xs = x[tok]
+
+    def gemms():
+        gu = torch._grouped_mm(xs, wgu, offs=offs)
+        h = torch.nn.functional.silu(gu[:, :f]) * gu[:, f:]
+        return torch._grouped_mm(h, wd, offs=offs)
+
+    def block():
+        o = gemms() * wr
+        y = torch.zeros(T, d, dtype=torch.float32, device=x.device).index_add_(0, tok, o.float())
+        for s in range(S):
+            g = x @ Wt[E + s][0].t()
+            u = x @ Wt[E + s][1].t()
+            ys = (torch.nn.functional.silu(g) * u) @ Wt[E + s][2].t()
+            y += ys.float() * (sw[:, s:s + 1] if sw is not None else 1.0)
+        return y.to(torch.bfloat16)
+
+    for _ in range(3):
+        block()
+    return time_steps(block, steps, flush), time_steps(gemms, steps, flush)
 
 
 def dist_init(n):
@@ -206,10 +267,17 @@ def main():
     table = table_for(cfg, args.table, T)
     weights = gen_weights(cfg)
     Wt = [[to_bf16(b, dev) for b in blk] for blk in weights]
-    layer = mx.MoELayer.from_weights(cfg.n_routed, cfg.n_shared, cfg.hidden, cfg.inter, cfg.shared_inter, Wt,
-                                     [[mx.Scheme.of(s) for s in row] for row in table])
+    use_ep = ws > 1 and not args.replicas
+    if use_ep:
+        from paper_2505_05799_b200.ep import ExpertParallelMoE
+        ep = ExpertParallelMoE.from_weights(cfg.n_routed, cfg.n_shared, cfg.hidden, cfg.inter, cfg.shared_inter, Wt,
+                                            table)
+        layer = ep.local  # the rank's routed experts: the dominant kernel
+    else:
+        layer = mx.MoELayer.from_weights(cfg.n_routed, cfg.n_shared, cfg.hidden, cfg.inter, cfg.shared_inter, Wt,
+                                         [[mx.Scheme.of(s) for s in row] for row in table])
     del Wt
-    # per-rank batch (replicas): rank r uses seeds offset by r
+    # per-rank batch: rank r uses seeds offset by r
     x_np = gen_activations(T, cfg.hidden, seed=1 + rank)
     ids_np, w_np = gen_routing(T, cfg.n_routed, cfg.top_k, seed=rank)
     sw_np = gen_shared_weights(T, cfg.n_shared, seed=2 + rank) if cfg.n_shared else None
@@ -218,16 +286,32 @@ def main():
     w = torch.from_numpy(w_np).to(dev)
     sw = torch.from_numpy(sw_np).to(dev) if sw_np is not None else None
     k = cfg.top_k
-    wsb = layer.workspace(T, k)
     y = torch.empty(T, cfg.hidden, dtype=torch.bfloat16, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    if use_ep:
+        def step(xa, ia, wa, sa, out):
+            out.copy_(ep(xa, ia, wa, sa))
+        wsb = None
+        # the local layer's counts: every rank's routing restricted to this rank's experts (host, seeded)
+        epr = cfg.n_routed // ws
+        all_ids = np.concatenate([gen_routing(T, cfg.n_routed, cfg.top_k, seed=r)[0] for r in range(ws)])
+        loc = all_ids[(all_ids >= rank * epr) & (all_ids < (rank + 1) * epr)] - rank * epr
+        counts_local = np.bincount(loc, minlength=epr)
+    else:
+        wsb = layer.workspace(T, k)
+
+        def step(xa, ia, wa, sa, out):
+            layer(xa, ia, wa, sa, out=out, workspace=wsb)
 
     for _ in range(args.warmup):
-        layer(x, ids, w, sw, out=y, workspace=wsb)
+        step(x, ids, w, sw, y)
     torch.cuda.synchronize()
-    assert layer.poll_error(wsb) == 0
-    n_tasks, n_exec = layer.task_stats(T, k, wsb)
-    assert n_tasks == n_exec and n_tasks > 0, (n_tasks, n_exec)
+    if not use_ep:
+        assert layer.poll_error(wsb) == 0
+        n_tasks, n_exec = layer.task_stats(T, k, wsb)
+        assert n_tasks == n_exec and n_tasks > 0, (n_tasks, n_exec)
+    else:
+        n_tasks = None
 
     K = args.steps
     layer.profile(K)
@@ -238,7 +322,7 @@ def main():
     for i in range(K):
         flush.zero_()
         ev[i][0].record()
-        layer(x, ids, w, sw, out=y, workspace=wsb)
+        step(x, ids, w, sw, y)
         ev[i][1].record()
     barrier(ws)
     clocks = clk.stop()
@@ -269,7 +353,7 @@ def main():
             wd.copy_(wh, non_blocking=True)
             if swd is not None:
                 swd.copy_(swh, non_blocking=True)
-            layer(xd, idd, wd, swd, out=y, workspace=wsb)
+            step(xd, idd, wd, swd, y)
             yh.copy_(y, non_blocking=True)
             ev2[i][1].record()
         barrier(ws)
@@ -280,8 +364,11 @@ def main():
 
     # ---- roofline of the dominant kernel (the persistent group-GEMM)
     peaks = load_peaks()
-    counts = np.bincount(ids_np[ids_np >= 0].reshape(-1), minlength=cfg.n_routed)
-    rl = layer_roofline(table, counts, cfg.hidden, cfg.inter, cfg.shared_inter, cfg.n_routed, T, peaks)
+    if use_ep:  # the local layer: this rank's experts (no shared) on the rows it received
+        rl = layer_roofline(table[rank * epr:(rank + 1) * epr], counts_local, cfg.hidden, cfg.inter, 0, epr, T, peaks)
+    else:
+        counts = np.bincount(ids_np[ids_np >= 0].reshape(-1), minlength=cfg.n_routed)
+        rl = layer_roofline(table, counts, cfg.hidden, cfg.inter, cfg.shared_inter, cfg.n_routed, T, peaks)
     i8_dom = rl["flops_i8"] > rl["flops_bf16"]
     peak_tf = peaks["i8_tops"] if i8_dom else peaks["bf16_tflops"]
     achieved = rl["flops"] / (gemm_ms / 1e3) / 1e12
@@ -299,6 +386,31 @@ def main():
                   "frac_of_step": rl["t_roof"] / (ms / 1e3), "alg_bytes": rl["bytes"]}
     stage_ms = {n: float(stages[:, i].mean()) for i, n in enumerate(["route", "gather", "plan", "gemm", "combine"])}
 
+    comparators = None
+    if not args.no_comparators and args.table == "mixed" and ws == 1:
+        comparators = {"note": "same routing and tokens; ms per block step, L2 flushed; tokens/s = T / time"}
+        Wt = [[to_bf16(b, dev) for b in blk] for blk in weights]
+        try:
+            blk_ms, gemm_ms_bf16 = bf16_grouped_block(cfg, Wt, x, ids, w, sw, K, flush)
+            comparators["bf16_torch_grouped_mm"] = {"block_ms": blk_ms, "gemm_ms": gemm_ms_bf16,
+                                                    "tokens_per_s": T / (blk_ms / 1e3)}
+        except Exception as e:  # comparator failures never fail the bench
+            comparators["bf16_torch_grouped_mm"] = {"error": str(e)[:200]}
+        for tb in UNIFORM_COMPARATORS.get(cfg.name, []):
+            tab_u = table_for(cfg, tb, T)
+            lay = mx.MoELayer.from_weights(cfg.n_routed, cfg.n_shared, cfg.hidden, cfg.inter, cfg.shared_inter, Wt,
+                                           [[mx.Scheme.of(sc) for sc in row] for row in tab_u])
+            wsu = lay.workspace(T, k)
+            for _ in range(3):
+                lay(x, ids, w, sw, out=y, workspace=wsu)
+            lay.profile(K)
+            u_ms = time_steps(lambda: lay(x, ids, w, sw, out=y, workspace=wsu), K, flush)
+            u_gemm = float(lay.profile_read(K)[:, 3].mean())
+            comparators["ours_uniform_" + tb] = {"block_ms": u_ms, "gemm_ms": u_gemm, "tokens_per_s": T / (u_ms / 1e3)}
+            del lay, wsu
+        del Wt
+        comparators["ours_mixed"] = {"block_ms": ms, "gemm_ms": gemm_ms, "tokens_per_s": T / (ms / 1e3)}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         samp = min(T, args.cpu_sample)
@@ -306,6 +418,9 @@ def main():
         cpu = {"value": tps, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                "sample": f"first {samp} tokens of the {cfg.name} T={T} batch (oracle.moe.moe_block, fp64), "
                          f"{dt:.1f} s"}
+    launches = layer.kernels_per_call
+    if use_ep:  # ep_route + ep_pack + local layer + shared layer + ep_combine (NCCL kernels not counted)
+        launches += 3 + (ep.shared.kernels_per_call if ep.shared is not None else 0)
     if rank == 0:
         dt = "int8" if i8_dom else "bf16"
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
@@ -314,9 +429,10 @@ def main():
                 "config": {"workload": cfg.name, "tokens_per_gpu": T, "experts": f"{cfg.n_routed}+{cfg.n_shared}",
                            "hidden": cfg.hidden, "inter": cfg.inter, "top_k": k, "table": args.table,
                            "l2": "flushed before every timed step (256 MB memset, untimed)",
-                           "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+                           "parallelism": (f"ep{ws} (NCCL all-to-all dispatch/combine, shared experts replicated)"
+                                           if use_ep else f"replicas x{ws}") if ws > 1 else "single GPU"},
                 "roofline": roofline, "per_expert_roofline": per_expert, "stage_ms": stage_ms,
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": layer.kernels_per_call * K, "clocks": clocks,
+                "cpu_baseline": cpu, "e2e": e2e, "comparators": comparators, "gpu_launches": launches * K, "clocks": clocks,
                 "tasks_per_step": n_tasks}
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -150,6 +150,26 @@ mxm_status mxm_layer_debug_counters(mxm_layer* l, void* dev_buf);
 /* Number of library kernels one mxm_moe_group_gemm call launches (route x3-4, gather, plan, GEMM, combine). */
 int32_t mxm_kernels_per_call(const mxm_layer* l);
 
+/* ---------------------------------------------------------------- expert parallelism
+ * Rank r of G owns routed experts [r*E/G, (r+1)*E/G); tokens stay on their source rank. The host runtime
+ * exchanges counts and rows with NCCL all-to-all(v) (torch.distributed on ProcessGroupNCCL); these calls
+ * build the send buffers and combine the returned partial sums. All pointers are device pointers.
+ *
+ * [async] per destination rank: how many of this rank's T tokens have >= 1 routed expert there (dedup),
+ *   dest_counts int32[G]; pos int32[T, G] = stable slot of token t in destination r's block, or -1. */
+mxm_status mxm_ep_route(const int32_t* topk_ids, int64_t T, int32_t k, int32_t E, int32_t G, int32_t* dest_counts,
+                        int32_t* pos, int32_t* err, mxm_stream stream);
+/* [async] send rows ordered by (destination, token): send_x bf16 [S, d] (S = sum dest_counts), send_ids int32
+ *   [S, k] local expert ids (id - r*E/G) or -1 for experts hosted elsewhere, send_w f32 [S, k], send_src int32 [S].
+ *   dest_offsets int32[G+1] = exclusive scan of dest_counts (device). */
+mxm_status mxm_ep_pack(const void* x, int64_t T, int32_t d, const int32_t* topk_ids, const float* topk_w, int32_t k,
+                       int32_t E, int32_t G, const int32_t* pos, const int32_t* dest_offsets, void* send_x,
+                       int32_t* send_ids, float* send_w, int32_t* send_src, mxm_stream stream);
+/* [async] y[t] = bf16( sum over destinations r ascending of back[dest_offsets[r] + pos[t, r]] + y_shared[t] );
+ *   back bf16 [S, d] = partial block outputs returned in send order; y_shared bf16 [T, d] or NULL. */
+mxm_status mxm_ep_combine(const void* back, const int32_t* pos, const int32_t* dest_offsets, int32_t G, int64_t T,
+                          int32_t d, const void* y_shared, void* y, mxm_stream stream);
+
 /* Thread-local message for the last error returned on this thread. */
 const char* mxm_last_error(void);
 /* Library version string. */

@@ -59,6 +59,9 @@ SIGNATURES = {
     "mxm_layer_profile_read": (C.c_int, [_P, _P, _I32, C.POINTER(_I32)]),
     "mxm_kernels_per_call": (C.c_int32, [_P]),
     "mxm_layer_debug_counters": (C.c_int, [_P, _P]),
+    "mxm_ep_route": (C.c_int, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "mxm_ep_pack": (C.c_int, [_P, _I64, _I32, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
+    "mxm_ep_combine": (C.c_int, [_P, _P, _P, _I32, _I64, _I32, _P, _P, _P]),
     "mxm_last_error": (C.c_char_p, []),
     "mxm_version": (C.c_char_p, []),
 }

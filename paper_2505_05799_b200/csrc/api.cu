@@ -433,6 +433,33 @@ mxm_status mxm_layer_debug_counters(mxm_layer* l, void* dev_buf) {
 
 int32_t mxm_kernels_per_call(const mxm_layer* l) { return l ? 7 + (l->S > 0 ? 1 : 0) : 0; }
 
+mxm_status mxm_ep_route(const int32_t* topk_ids, int64_t T, int32_t k, int32_t E, int32_t G, int32_t* dest_counts,
+                        int32_t* pos, int32_t* err, mxm_stream stream) {
+  if (!topk_ids || !dest_counts || !pos) return fail(MXM_E_CONFIG, "null argument");
+  if (G <= 0 || G > 64 || E % G != 0 || k <= 0 || k > 32 || T < 0) return fail(MXM_E_CONFIG, "bad E/G/k/T");
+  MXM_CUDA(launch_ep_route(topk_ids, T, k, E, G, dest_counts, pos, err, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_ep_pack(const void* x, int64_t T, int32_t d, const int32_t* topk_ids, const float* topk_w, int32_t k,
+                       int32_t E, int32_t G, const int32_t* pos, const int32_t* dest_offsets, void* send_x,
+                       int32_t* send_ids, float* send_w, int32_t* send_src, mxm_stream stream) {
+  if (!x || !topk_ids || !topk_w || !pos || !dest_offsets || !send_x || !send_ids || !send_w || !send_src)
+    return fail(MXM_E_CONFIG, "null argument");
+  if (G <= 0 || E % G != 0 || d % 8 != 0 || k > 32) return fail(MXM_E_CONFIG, "bad shape");
+  MXM_CUDA(launch_ep_pack(x, T, d, topk_ids, topk_w, k, E, G, pos, dest_offsets, send_x, send_ids, send_w, send_src,
+                          (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_ep_combine(const void* back, const int32_t* pos, const int32_t* dest_offsets, int32_t G, int64_t T,
+                          int32_t d, const void* y_shared, void* y, mxm_stream stream) {
+  if (!back || !pos || !dest_offsets || !y) return fail(MXM_E_CONFIG, "null argument");
+  if (G <= 0 || d % 8 != 0) return fail(MXM_E_CONFIG, "bad shape");
+  MXM_CUDA(launch_ep_combine(back, pos, dest_offsets, G, T, d, y_shared, y, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
 mxm_status mxm_poll_device_error(const mxm_layer* l, const void* ws, mxm_stream stream, int32_t* code) {
   if (!l || !ws || !code) return fail(MXM_E_CONFIG, "null argument");
   int32_t v = 0;

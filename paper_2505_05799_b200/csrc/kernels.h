@@ -50,5 +50,12 @@ cudaError_t launch_plan(const ExpertDesc* ex, int V, int E, int64_t T, int d, co
                         int64_t task_cap, Task* tasks, int32_t* meta, int32_t* grp_n1, int32_t* grp_nq,
                         int32_t* p1_done, int32_t* hq_done, cudaStream_t st);
 cudaError_t launch_moe_gemm(const GemmParams& prm, int grid, cudaStream_t st);
+cudaError_t launch_ep_route(const int32_t* ids, int64_t T, int k, int E, int G, int32_t* dest_counts, int32_t* pos,
+                            int32_t* err, cudaStream_t st);
+cudaError_t launch_ep_pack(const void* x, int64_t T, int d, const int32_t* ids, const float* w, int k, int E, int G,
+                           const int32_t* pos, const int32_t* dest_off, void* sx, int32_t* sids, float* sw,
+                           int32_t* ssrc, cudaStream_t st);
+cudaError_t launch_ep_combine(const void* back, const int32_t* pos, const int32_t* dest_off, int G, int64_t T, int d,
+                              const void* ysh, void* y, cudaStream_t st);
 
 }  // namespace mxm

@@ -1,0 +1,121 @@
+"""Expert-parallel MoE block over a torch.distributed process group.
+
+Eq. 2 is a sum over experts, so the block shards by experts: rank r of G owns
+routed experts [r·E/G, (r+1)·E/G); tokens stay data-parallel on their source rank; shared experts
+are replicated and run on each rank's own tokens.
+
+Per call (one NCCL all-to-all for counts, then all-to-all-v for rows; host sync for split sizes):
+  1. mxm_ep_route   per-destination dedup counts + stable slots        (kernel)
+  2. all_to_all     counts                                              (NCCL)
+  3. mxm_ep_pack    send rows + local (expert id, weight) metadata      (kernel)
+  4. all_to_all_v   rows, ids, weights                                  (NCCL)
+  5. local routed layer on the received rows (mxm_moe_group_gemm)       (kernels)
+  6. all_to_all_v   partial outputs back, in send order                 (NCCL)
+  7. shared experts on the own tokens (mxm_moe_group_gemm, top-k = S)   (kernels)
+  8. mxm_ep_combine fixed-order sum over destinations + shared          (kernel)
+Index math and arithmetic run in libmxmoe kernels; this module only sizes buffers and issues the
+collectives. `ops` and the two layers are injectable so the orchestration can be exercised with the
+gloo backend on CPU (tests/test_ep_gloo.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import MoELayer, Scheme, _ptr, _stream, check, load
+
+
+class CudaEpOps:
+    """The libmxmoe EP kernels (device tensors)."""
+
+    def route(self, ids: torch.Tensor, E: int, G: int):
+        T, k = ids.shape
+        counts = torch.zeros(G, dtype=torch.int32, device=ids.device)
+        pos = torch.empty(T, G, dtype=torch.int32, device=ids.device)
+        check(load().mxm_ep_route(_ptr(ids), T, k, E, G, _ptr(counts), _ptr(pos), None, _stream()))
+        return counts, pos
+
+    def pack(self, x, ids, w, pos, dest_off, E, G, S_total):
+        T, k = ids.shape
+        d = x.shape[1]
+        dev = x.device
+        sx = torch.empty(S_total, d, dtype=torch.bfloat16, device=dev)
+        sids = torch.empty(S_total, k, dtype=torch.int32, device=dev)
+        sw = torch.empty(S_total, k, dtype=torch.float32, device=dev)
+        ssrc = torch.empty(S_total, dtype=torch.int32, device=dev)
+        check(load().mxm_ep_pack(_ptr(x), T, d, _ptr(ids), _ptr(w), k, E, G, _ptr(pos), _ptr(dest_off), _ptr(sx),
+                                 _ptr(sids), _ptr(sw), _ptr(ssrc), _stream()))
+        return sx, sids, sw, ssrc
+
+    def combine(self, back, pos, dest_off, G, ysh, T, d):
+        y = torch.empty(T, d, dtype=torch.bfloat16, device=pos.device)
+        check(load().mxm_ep_combine(_ptr(back), _ptr(pos), _ptr(dest_off), G, T, d, _ptr(ysh), _ptr(y), _stream()))
+        return y
+
+
+class ExpertParallelMoE:
+    """One MoE layer sharded by experts over `group` (rank r owns routed experts [r·E/G, (r+1)·E/G))."""
+
+    def __init__(self, n_routed: int, hidden: int, local_layer: Callable, shared_layer: Optional[Callable],
+                 n_shared: int, group=None, ops=None):
+        self.group = group
+        self.G = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if n_routed % self.G:
+            raise ValueError("n_routed must be divisible by the expert-parallel world size")
+        self.E, self.S, self.d = n_routed, n_shared, hidden
+        self.local, self.shared = local_layer, shared_layer
+        self.ops = ops if ops is not None else CudaEpOps()
+
+    @classmethod
+    def from_weights(cls, n_routed: int, n_shared: int, hidden: int, inter: int, shared_inter: int,
+                     weights: Sequence[Sequence[torch.Tensor]], table, group=None) -> "ExpertParallelMoE":
+        """weights/table cover all routed experts then the shared ones (as in MoELayer.from_weights);
+        only this rank's experts (and the shared ones) are quantized and kept."""
+        G, r = dist.get_world_size(group), dist.get_rank(group)
+        epr = n_routed // G
+        lo = r * epr
+        local = MoELayer.from_weights(epr, 0, hidden, inter, 0, weights[lo:lo + epr],
+                                      [[Scheme.of(s) for s in row] for row in table[lo:lo + epr]])
+        shared = None
+        if n_shared:
+            shared = MoELayer.from_weights(n_shared, 0, hidden, shared_inter, 0, weights[n_routed:],
+                                           [[Scheme.of(s) for s in row] for row in table[n_routed:]])
+        return cls(n_routed, hidden, local, shared, n_shared, group)
+
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits):
+        dist.all_to_all_single(out, inp.contiguous(), out_splits, in_splits, group=self.group)
+
+    def __call__(self, x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor,
+                 shared_w: Optional[torch.Tensor] = None) -> torch.Tensor:
+        T, k = topk_ids.shape
+        G, E, d, dev = self.G, self.E, self.d, x.device
+        counts, pos = self.ops.route(topk_ids, E, G)
+        recv_counts = torch.empty_like(counts)
+        dist.all_to_all_single(recv_counts, counts, group=self.group)
+        send_splits = counts.tolist()  # host sync (v1): split sizes of the all-to-all-v
+        recv_splits = recv_counts.tolist()
+        dest_off_l = [0]
+        for c in send_splits:
+            dest_off_l.append(dest_off_l[-1] + c)
+        dest_off = torch.tensor(dest_off_l, dtype=torch.int32, device=dev)
+        sx, sids, sw, _ = self.ops.pack(x, topk_ids, topk_w, pos, dest_off, E, G, dest_off_l[-1])
+        R = sum(recv_splits)
+        rx = torch.empty(R, d, dtype=x.dtype, device=dev)
+        rids = torch.empty(R, k, dtype=torch.int32, device=dev)
+        rw = torch.empty(R, k, dtype=torch.float32, device=dev)
+        self._a2a(rx, sx, recv_splits, send_splits)
+        self._a2a(rids, sids, recv_splits, send_splits)
+        self._a2a(rw, sw, recv_splits, send_splits)
+        ry = self.local(rx, rids, rw) if R > 0 else torch.empty(0, d, dtype=x.dtype, device=dev)
+        back = torch.empty(dest_off_l[-1], d, dtype=x.dtype, device=dev)
+        self._a2a(back, ry, send_splits, recv_splits)
+        ysh = None
+        if self.S:
+            sid = torch.arange(self.S, dtype=torch.int32, device=dev).repeat(T, 1)
+            swt = shared_w if shared_w is not None else torch.ones(T, self.S, dtype=torch.float32, device=dev)
+            ysh = self.shared(x, sid, swt.contiguous())
+        return self.ops.combine(back, pos, dest_off, G, ysh, T, d)

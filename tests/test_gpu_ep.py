@@ -1,0 +1,103 @@
+"""Expert-parallel kernels on one GPU: index semantics vs the torch reference, and a loopback emulation of
+G ranks (all-to-all = tensor slicing) through the real mxm_ep_* kernels and per-rank layers, compared to
+the unsharded layer and to the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from synth import configs as C
+from tests.moe_cases import bf16_tensor, make_case, oracle_layer, oracle_run, row_rel_err
+from tests.test_ep_gloo import TorchRefEpOps
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mx():
+    import paper_2505_05799_b200 as mx
+    mx.load()
+    return mx
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_ep_kernels_match_reference(mx, G):
+    from paper_2505_05799_b200.ep import CudaEpOps
+    rng = np.random.default_rng(G)
+    T, k, E, d = 300, 4, 8, 256
+    ids = rng.integers(-1, E, (T, k)).astype(np.int32)
+    w = rng.random((T, k)).astype(np.float32)
+    x = torch.randn(T, d).to(torch.bfloat16)
+    ops, ref = CudaEpOps(), TorchRefEpOps()
+    c_g, p_g = ops.route(torch.from_numpy(ids).cuda(), E, G)
+    c_r, p_r = ref.route(torch.from_numpy(ids), E, G)
+    assert c_g.cpu().tolist() == c_r.tolist() and torch.equal(p_g.cpu(), p_r)
+    off = [0]
+    for c in c_r.tolist():
+        off.append(off[-1] + c)
+    off_t = torch.tensor(off, dtype=torch.int32)
+    sg = ops.pack(x.cuda(), torch.from_numpy(ids).cuda(), torch.from_numpy(w).cuda(), p_g, off_t.cuda(), E, G, off[-1])
+    sr = ref.pack(x, torch.from_numpy(ids), torch.from_numpy(w), p_r, off_t, E, G, off[-1])
+    for a, b in zip(sg, sr):
+        assert torch.equal(a.cpu(), b)
+    back = torch.randn(off[-1], d).to(torch.bfloat16)
+    ysh = torch.randn(T, d).to(torch.bfloat16)
+    yg = ops.combine(back.cuda(), p_g, off_t.cuda(), G, ysh.cuda(), T, d)
+    yr = ref.combine(back, p_r, off_t, G, ysh, T, d)
+    assert torch.equal(yg.cpu(), yr)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_ep_loopback_equals_unsharded(mx, G):
+    """G virtual ranks in one process: same kernels and layers as the NCCL path, all-to-all by slicing."""
+    from paper_2505_05799_b200.ep import CudaEpOps
+    cfg = C.get_config("dsv2")
+    table = C.precision_table(cfg)
+    T = 256
+    case = make_case(cfg, table, T, seed=5)
+    W = [[bf16_tensor(b) for b in blk] for blk in case["weights"]]
+    tab = [[mx.Scheme.of(s) for s in row] for row in table]
+    E, S, d = cfg.n_routed, cfg.n_shared, cfg.hidden
+    epr = E // G
+    locals_ = [mx.MoELayer.from_weights(epr, 0, d, cfg.inter, 0, W[r * epr:(r + 1) * epr], tab[r * epr:(r + 1) * epr])
+               for r in range(G)]
+    shared = mx.MoELayer.from_weights(S, 0, d, cfg.shared_inter, 0, W[E:], tab[E:])
+    ops = CudaEpOps()
+    Tr = T // G
+    xs = [bf16_tensor(case["x"][r * Tr:(r + 1) * Tr]) for r in range(G)]
+    ids = [torch.from_numpy(case["ids"][r * Tr:(r + 1) * Tr]).cuda() for r in range(G)]
+    ws = [torch.from_numpy(case["w"][r * Tr:(r + 1) * Tr]).cuda() for r in range(G)]
+    sws = [torch.from_numpy(case["shared_w"][r * Tr:(r + 1) * Tr]).cuda() for r in range(G)]
+    route = [ops.route(ids[r], E, G) for r in range(G)]
+    offs = []
+    packs = []
+    for r in range(G):
+        c = route[r][0].cpu().tolist()
+        off = [0]
+        for v in c:
+            off.append(off[-1] + v)
+        offs.append(off)
+        packs.append(ops.pack(xs[r], ids[r], ws[r], route[r][1], torch.tensor(off, dtype=torch.int32).cuda(), E, G,
+                              off[-1]))
+    # all-to-all: destination q receives the block for q from every source r (in source order)
+    outs = {}
+    for q in range(G):
+        parts = [(r, offs[r][q], offs[r][q + 1]) for r in range(G)]
+        rx = torch.cat([packs[r][0][a:b] for r, a, b in parts])
+        rid = torch.cat([packs[r][1][a:b] for r, a, b in parts])
+        rw = torch.cat([packs[r][2][a:b] for r, a, b in parts])
+        ry = locals_[q](rx.contiguous(), rid.contiguous(), rw.contiguous())
+        n = 0
+        for r, a, b in parts:
+            outs[(r, q)] = ry[n:n + (b - a)]
+            n += b - a
+    ys = []
+    for r in range(G):
+        back = torch.cat([outs[(r, q)] for q in range(G)])
+        sid = torch.arange(S, dtype=torch.int32, device="cuda").repeat(Tr, 1)
+        ysh = shared(xs[r], sid, sws[r])
+        ys.append(ops.combine(back.contiguous(), route[r][1], torch.tensor(offs[r], dtype=torch.int32).cuda(), G, ysh,
+                              Tr, d))
+    y = torch.cat(ys).float().cpu().numpy().astype(np.float64)
+    rows = np.arange(0, T, 4)
+    ref = oracle_run(oracle_layer(case), case, rows=rows)
+    assert row_rel_err(y[rows], ref) <= 1e-2
