@@ -74,6 +74,8 @@ def load(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    # experiment variants built in-tree by build.build_variant (tools/); default: the product library
+    path = os.environ.get("MXM_LIB", path)
     if not os.path.exists(path):
         raise MxmError(MXM_E_CUDA, f"{path} not built; run __graft_entry__.build() (no CPU fallback exists)")
     lib = C.CDLL(path)

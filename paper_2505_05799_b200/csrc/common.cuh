@@ -73,6 +73,23 @@ struct Task {
 };
 static_assert(sizeof(Task) == 16, "task size");
 
+// Token-tile cap of an expert's m-tiles: dual gate/up tiles of up to 96 tokens fit one 192-column TMEM
+// accumulator buffer; register-accumulated tiles (g128 W-A dual, or gate and up as two sub-loops) keep
+// 64 columns per warpgroup half in registers -> 64 tokens.
+__host__ __device__ inline int tile_cap(const ExpertDesc& e) {
+  const bool reg = !e.dual || (kind_is_i8(e.blk[0].geo.kind) && e.blk[0].geo.group == 128);
+  return reg ? 64 : 96;
+}
+// Down tasks pair two 128-channel output tiles (two mats sharing the h tile) unless the down is a g128
+// W-A block whose register-accumulated drain would exceed 64 columns per thread.
+__host__ __device__ inline bool down_pair(const ExpertDesc& e, int nt, int nd) {
+  const bool g128 = kind_is_i8(e.blk[2].geo.kind) && e.blk[2].geo.group == 128;
+  return nd >= 2 && !(g128 && nt > 64);
+}
+__host__ __device__ inline int down_tasks(const ExpertDesc& e, int nt, int nd) {
+  return down_pair(e, nt, nd) ? (nd + 1) / 2 : nd;
+}
+
 }  // namespace mxm
 
 namespace mxm {

@@ -29,36 +29,48 @@ namespace mxm {
 
 constexpr int kStages = 4;
 constexpr int kRing = 4;
-constexpr int kAccBufs = 2;      // accumulator buffers of 128 TMEM columns at [0, 256)
-constexpr int kTmemA = 256;      // TMEM A ring (dequantized weights, TS-form MMA): 4 stages x 2 mats x 32 columns
-constexpr int kThreads = 512;  // 16 warps: producer, 2 MMA issuers, idle, 4 transform, 8 epilogue
-constexpr int kXfWarps = 4;     // transform warps 4..7 (one A row = one TMEM lane per thread)
+// TMEM (512 columns): two accumulator buffers of 192 columns at [0, 384) -- a dual tile (gate | up, or two
+// 128-channel down tiles) of up to 96 tokens fits one buffer, so every task is double-buffered against the
+// next one's MMAs -- and a 2-slot A ring at [384, 512) for TS-form MMAs (dequantized weights; per slot
+// 2 mats x 32 columns), decoupled from the 4 smem stages by its own ready / empty barriers.
+constexpr int kAccBufs = 2;
+constexpr int kAccCols = 192;
+constexpr int kMat1Col = 96;     // column offset of mat 1 inside an accumulator buffer
+constexpr int kTmemA = kAccBufs * kAccCols;
+constexpr int kASlots = 2;
+constexpr int kThreads = 640;  // 20 warps: producer, MMA issuer, 2 idle, 4 transform, 8 epilogue, 4 transform
+constexpr int kXfWarps = 8;     // transform warps 4..7 (K half 0) and 16..19 (K half 1); one A row per thread
 constexpr int kTileBytes = 16384;
 constexpr int kSlotBytes = 3 * kTileBytes;  // per stage: token tile B | mat 0 (raw codes or A image) | mat 1
 
 constexpr int kOffCtl = kStages * kSlotBytes;
-constexpr int kCtlBytes = 1024;
+constexpr int kCtlBytes = 4096;
 constexpr int kSmemBytes = kOffCtl + kCtlBytes + 1024;
 
 struct Ctl {
-  uint64_t full[kStages], empty[kStages], aready[kStages];
+  uint64_t full[kStages], empty[kStages];
+  uint64_t aready[kASlots], aempty[kASlots];
   uint64_t accf[kAccBufs], acce[kAccBufs];
   uint64_t tfull[kRing], tempty[kRing];
   Task ring[kRing];
   uint32_t tmem_base;
   uint32_t colmax[2][2][4][8];  // [buffer][warpgroup][lane quarter][column] for the fused g128 h-quant
+  alignas(16) float sa[8][64];  // per epilogue warp: activation scales of the current drain event
 };
 static_assert(sizeof(Ctl) <= kCtlBytes, "ctl");
 
 struct SubLoop {
   const LinDesc* mat[2];
+  int tile[2];                           // 128-channel output tile of each mat
   int nmats, bmap, ns, i8, xform, g128;  // xform: bit m set = mat m needs the packed->A transform
 };
 
-__device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, int bmap) {
+__device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, int bmap, int tile0, int tile1) {
   SubLoop s;
   s.mat[0] = a;
   s.mat[1] = b;
+  s.tile[0] = tile0;
+  s.tile[1] = tile1;
   s.nmats = b ? 2 : 1;
   s.bmap = bmap;
   s.ns = a->geo.ns;
@@ -68,18 +80,27 @@ __device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, i
   return s;
 }
 
-__device__ __forceinline__ int build_subloops(const Task& t, const ExpertDesc* __restrict__ ex, SubLoop* sl) {
+// phase 0: gate & up share the token tile (one sub-loop when dual); phase 2: a task covers down tiles
+// (2j, 2j+1) as two mats sharing the h tile when down_pair() (common.cuh), else tile j alone
+__device__ __forceinline__ int build_subloops(const Task& t, const ExpertDesc* __restrict__ ex, int d, SubLoop* sl) {
   const ExpertDesc& e = ex[t.expert];
   if (t.phase == 0) {
     if (e.dual) {
-      sl[0] = make_sl(&e.blk[0], &e.blk[1], e.blk[0].in_slot);
+      sl[0] = make_sl(&e.blk[0], &e.blk[1], e.blk[0].in_slot, t.ntile, t.ntile);
       return 1;
     }
-    sl[0] = make_sl(&e.blk[0], nullptr, e.blk[0].in_slot);
-    sl[1] = make_sl(&e.blk[1], nullptr, e.blk[1].in_slot);
+    sl[0] = make_sl(&e.blk[0], nullptr, e.blk[0].in_slot, t.ntile, t.ntile);
+    sl[1] = make_sl(&e.blk[1], nullptr, e.blk[1].in_slot, t.ntile, t.ntile);
     return 2;
   }
-  sl[0] = make_sl(&e.blk[2], nullptr, 3 + e.blk[2].in_slot);
+  const int nd = d / 128;
+  if (down_pair(e, t.nt, nd)) {
+    const int j0 = 2 * t.ntile;
+    const bool two = j0 + 1 < nd;
+    sl[0] = make_sl(&e.blk[2], two ? &e.blk[2] : nullptr, 3 + e.blk[2].in_slot, j0, j0 + 1);
+  } else {
+    sl[0] = make_sl(&e.blk[2], nullptr, 3 + e.blk[2].in_slot, t.ntile, t.ntile);
+  }
   return 1;
 }
 
@@ -99,15 +120,20 @@ __device__ __forceinline__ uint32_t bf2_fma(uint32_t a, uint32_t b, uint32_t c) 
 }
 // (128 + u_even, 128 + u_odd) as bf16x2 -> q*s + z rounded once to bf16 (q = u - off)
 __device__ __forceinline__ uint32_t deq_pair(uint32_t fields, uint32_t off2, uint32_t s2, uint32_t z2) {
-  return bf2_fma(bf2_sub(fields | 0x43004300u, off2), s2, z2);
+  return bf2_fma(bf2_sub(fields, off2), s2, z2);
+}
+// codes of one pair at bits (sh, sh+16) of `word`, widths given by `mask`, as (128+u) bf16x2 (one LOP3)
+__device__ __forceinline__ uint32_t pair_fields(uint32_t word, int sh, uint32_t mask) {
+  return and_or(word >> sh, mask, 0x43004300u);
 }
 
-// Weight-only dequant of one A row (thread r = TMEM lane r): packed codes -> 64 bf16 = 32 words o[] in K order
-// (o[j] = elements 2j, 2j+1), later written to the TMEM A ring with one tcgen05.st.
+// Weight-only dequant of one half-stage of one A row (thread r = TMEM lane r): the H-th 32 of the stage's
+// 64 K elements -> 16 words o[] in K order (o[j] = elements 2j, 2j+1), written to the TMEM A ring with one
+// tcgen05.st (two transform warpgroups split every stage by K halves).
 // `hm`: this stage starts a group, so the chunk begins with scale[128] (and zero[128] if asymmetric).
-template <int BITS>
+template <int BITS, int H>
 __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, bool hm, int meta_bytes, bool sym,
-                                         uint32_t off2, int r, uint32_t& s2, uint32_t& z2, uint32_t (&o)[32]) {
+                                         uint32_t off2, int r, uint32_t& s2, uint32_t& z2, uint32_t (&o)[16]) {
   const uint8_t* codes = raw;
   if (hm) {
     const uint32_t sb = reinterpret_cast<const uint16_t*>(raw)[r];
@@ -123,35 +149,35 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, bool h
   const uint32_t* w = reinterpret_cast<const uint32_t*>(codes);
   if constexpr (BITS == 4) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t word = w[j * 128 + r];
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t word = w[(4 * H + j) * 128 + r];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) o[4 * j + t] = deq_pair((word >> (4 * t)) & 0x000F000Fu, off2, s2, z2);
+      for (int t = 0; t < 4; ++t) o[4 * j + t] = deq_pair(pair_fields(word, 4 * t, 0x000F000Fu), off2, s2, z2);
     }
   } else if constexpr (BITS == 2) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t word = w[j * 128 + r];
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t word = w[(2 * H + j) * 128 + r];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) o[8 * j + t] = deq_pair((word >> (2 * t)) & 0x00030003u, off2, s2, z2);
+      for (int t = 0; t < 8; ++t) o[8 * j + t] = deq_pair(pair_fields(word, 2 * t, 0x00030003u), off2, s2, z2);
     }
   } else if constexpr (BITS == 3) {
-    const uint32_t* wh = w + 4 * 128;
-    const uint32_t h0 = wh[r], h1 = wh[128 + r];
+    const uint32_t hw2 = w[(4 + H) * 128 + r];  // high-bit plane word covering low-plane words 2H, 2H+1
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t word = w[j * 128 + r];
-      const uint32_t hw = ((j >> 1) ? h1 : h0) >> (8 * (j & 1));
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t word = w[(2 * H + j) * 128 + r];
+      const uint32_t hw = hw2 >> (8 * j);
 #pragma unroll
       for (int t = 0; t < 8; ++t)
-        o[8 * j + t] = deq_pair(((word >> (2 * t)) & 0x00030003u) | (((hw >> t) & 0x00010001u) << 2), off2, s2, z2);
+        o[8 * j + t] = deq_pair(and_or(word >> (2 * t), 0x00030003u, (((hw >> t) & 0x00010001u) << 2) | 0x43004300u),
+                                off2, s2, z2);
     }
   } else {  // 8-bit: fp32 path (128 + u is not exact in bf16 for u >= 128)
     const float sf = __uint_as_float(s2 << 16), zf = __uint_as_float(z2 << 16);
     const float fo = (float)(off2 & 0xFFu);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t word = w[j * 128 + r];
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t word = w[(8 * H + j) * 128 + r];
       float f[4];
 #pragma unroll
       for (int b = 0; b < 4; ++b) f[b] = (__uint_as_float(0x4B000000u | ((word >> (8 * b)) & 0xFFu)) - 8388608.f) - fo;
@@ -163,44 +189,74 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, bool h
   }
 }
 
+template <int H>
 __device__ __forceinline__ void xform_wo_any(int bits, const uint8_t* raw, bool hm, int mb, bool sym, uint32_t off2,
-                                             int r, uint32_t& s2, uint32_t& z2, uint32_t (&o)[32]) {
+                                             int r, uint32_t& s2, uint32_t& z2, uint32_t (&o)[16]) {
   switch (bits) {
     case 2:
-      xform_wo<2>(raw, hm, mb, sym, off2, r, s2, z2, o);
+      xform_wo<2, H>(raw, hm, mb, sym, off2, r, s2, z2, o);
       break;
     case 3:
-      xform_wo<3>(raw, hm, mb, sym, off2, r, s2, z2, o);
+      xform_wo<3, H>(raw, hm, mb, sym, off2, r, s2, z2, o);
       break;
     case 4:
-      xform_wo<4>(raw, hm, mb, sym, off2, r, s2, z2, o);
+      xform_wo<4, H>(raw, hm, mb, sym, off2, r, s2, z2, o);
       break;
     default:
-      xform_wo<8>(raw, hm, mb, sym, off2, r, s2, z2, o);
+      xform_wo<8, H>(raw, hm, mb, sym, off2, r, s2, z2, o);
       break;
   }
 }
 
 __device__ __forceinline__ uint32_t to_s8_4(uint32_t u, uint32_t bias) { return (u + bias) ^ 0x80808080u; }
 
-// W-A w4/w5 unpack of one row: 128 codes -> s8, o[j] = bytes 4j..4j+3 in K order
-template <int BITS>
-__device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, int r, uint32_t (&o)[32]) {
+// W-A w4/w5 unpack of one half-stage of one row: 64 of the stage's 128 codes -> s8, o[j] = bytes 4j..4j+3
+template <int BITS, int H>
+__device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, int r, uint32_t (&o)[16]) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(raw);
   const uint32_t* wh = w + 16 * 128;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = 8 * H + jj;
     const uint32_t word = w[j * 128 + r];
     if constexpr (BITS == 4) {
-      o[2 * j] = to_s8_4(word & 0x0F0F0F0Fu, 0x78787878u);
-      o[2 * j + 1] = to_s8_4((word >> 4) & 0x0F0F0F0Fu, 0x78787878u);
+      o[2 * jj] = to_s8_4(word & 0x0F0F0F0Fu, 0x78787878u);
+      o[2 * jj + 1] = to_s8_4((word >> 4) & 0x0F0F0F0Fu, 0x78787878u);
     } else {
       const uint32_t hb = wh[(j >> 2) * 128 + r];
       const int t0 = 2 * (j & 3);
       const uint32_t lo = (word & 0x0F0F0F0Fu) | (((hb >> t0) & 0x01010101u) << 4);
       const uint32_t hi = ((word >> 4) & 0x0F0F0F0Fu) | (((hb >> (t0 + 1)) & 0x01010101u) << 4);
-      o[2 * j] = to_s8_4(lo, 0x70707070u);
-      o[2 * j + 1] = to_s8_4(hi, 0x70707070u);
+      o[2 * jj] = to_s8_4(lo, 0x70707070u);
+      o[2 * jj + 1] = to_s8_4(hi, 0x70707070u);
+    }
+  }
+}
+
+// one transform warpgroup's share (K half H) of one stage: both mats -> TMEM A ring
+template <int H>
+__device__ __forceinline__ void xform_stage(const SubLoop& s, const uint8_t* x0, const uint8_t* x1, uint32_t tA, int r,
+                                            bool hmA, bool hmB, int bitsA, int bitsB, int mbA, int mbB, bool symA,
+                                            bool symB, uint32_t offA, uint32_t offB, bool xa, bool xb, uint32_t& sa,
+                                            uint32_t& za, uint32_t& sb, uint32_t& zb) {
+  uint32_t o[16];
+  if (s.i8) {
+    if (xa) {
+      if (bitsA == 4) xform_wa<4, H>(x0, r, o); else xform_wa<5, H>(x0, r, o);
+      tmem_st16(tA + 16 * H, o);
+    }
+    if (xb) {
+      if (bitsB == 4) xform_wa<4, H>(x1, r, o); else xform_wa<5, H>(x1, r, o);
+      tmem_st16(tA + 32 + 16 * H, o);
+    }
+  } else {
+    if (xa) {
+      xform_wo_any<H>(bitsA, x0, hmA, mbA, symA, offA, r, sa, za, o);
+      tmem_st16(tA + 16 * H, o);
+    }
+    if (xb) {
+      xform_wo_any<H>(bitsB, x1, hmB, mbB, symB, offB, r, sb, zb, o);
+      tmem_st16(tA + 32 + 16 * H, o);
     }
   }
 }
@@ -242,35 +298,45 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // One drain event of the register-accumulating epilogue for HALF token columns of this warpgroup.
 // acc2 holds 64 fp32 accumulators as 32 pairs: dual gate/up -> gate cols in pairs [0,16), up in [16,32);
 // single -> cols in pairs [0,32). i8: acc += int32 * (s_w * s_a[col]) ; bf16-kind: acc += fp32.
+// `sa` is this warp's smem copy of the event's activation scales (broadcast reads, no shuffles).
+// SMALL (g128 groups: |int32| <= 128*127*127 < 2^22): exact int->float by the 2^23+2^22 magic add
+// (IADD + FADD on the full-rate pipes instead of the quarter-rate I2F).
 template <int HALF, int DST0>
 __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8, bool two,
-                                            float sw0, float sw1, float sa_lo, float sa_hi) {
+                                            bool small, float sw0, float sw1, const float* sa) {
   constexpr int CH = 8;
+  constexpr float kMagic = 12582912.f;  // 2^23 + 2^22
 #pragma unroll
   for (int c0 = 0; c0 < HALF; c0 += CH) {
-    uint32_t va[16], vb[16];
-    if constexpr (CH == 16) {
-      tmem_ld16(addrA + c0, va);
-      if (two) tmem_ld16(addrB + c0, vb);
-    } else {
-      uint32_t (&va8)[8] = *reinterpret_cast<uint32_t(*)[8]>(&va[0]);
-      uint32_t (&vb8)[8] = *reinterpret_cast<uint32_t(*)[8]>(&vb[0]);
-      tmem_ld8(addrA + c0, va8);
-      if (two) tmem_ld8(addrB + c0, vb8);
-    }
+    uint32_t va[8], vb[8];
+    tmem_ld8(addrA + c0, va);
+    if (two) tmem_ld8(addrB + c0, vb);
     tmem_ld_wait();
+    if (i8) {
+      const float4 s4a = *reinterpret_cast<const float4*>(sa + c0);
+      const float4 s4b = *reinterpret_cast<const float4*>(sa + c0 + 4);
+      const float2 sac[4] = {make_float2(s4a.x, s4a.y), make_float2(s4a.z, s4a.w), make_float2(s4b.x, s4b.y),
+                             make_float2(s4b.z, s4b.w)};
 #pragma unroll
-    for (int j = 0; j < CH; j += 2) {
-      const int col = c0 + j;
-      if (i8) {
-        const float2 sa = make_float2(colval(sa_lo, sa_hi, col), colval(sa_lo, sa_hi, col + 1));
-        const float2 fa = make_float2((float)(int32_t)va[j], (float)(int32_t)va[j + 1]);
-        acc2[DST0 + col / 2] = ffma2(fa, fmul2(make_float2(sw0, sw0), sa), acc2[DST0 + col / 2]);
-        if (two) {
-          const float2 fb = make_float2((float)(int32_t)vb[j], (float)(int32_t)vb[j + 1]);
-          acc2[16 + col / 2] = ffma2(fb, fmul2(make_float2(sw1, sw1), sa), acc2[16 + col / 2]);
+      for (int j = 0; j < CH; j += 2) {
+        const int col = c0 + j;
+        float2 fa, fb;
+        if (small) {
+          fa = fadd2(make_float2(__int_as_float((int32_t)va[j] + 0x4B400000), __int_as_float((int32_t)va[j + 1] + 0x4B400000)),
+                     make_float2(-kMagic, -kMagic));
+          fb = fadd2(make_float2(__int_as_float((int32_t)vb[j] + 0x4B400000), __int_as_float((int32_t)vb[j + 1] + 0x4B400000)),
+                     make_float2(-kMagic, -kMagic));
+        } else {
+          fa = make_float2((float)(int32_t)va[j], (float)(int32_t)va[j + 1]);
+          fb = make_float2((float)(int32_t)vb[j], (float)(int32_t)vb[j + 1]);
         }
-      } else {
+        acc2[DST0 + col / 2] = ffma2(fa, fmul2(make_float2(sw0, sw0), sac[j / 2]), acc2[DST0 + col / 2]);
+        if (two) acc2[16 + col / 2] = ffma2(fb, fmul2(make_float2(sw1, sw1), sac[j / 2]), acc2[16 + col / 2]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CH; j += 2) {
+        const int col = c0 + j;
         acc2[DST0 + col / 2] = fadd2(acc2[DST0 + col / 2], make_float2(__uint_as_float(va[j]), __uint_as_float(va[j + 1])));
         if (two)
           acc2[16 + col / 2] = fadd2(acc2[16 + col / 2], make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1])));
@@ -281,19 +347,22 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
 
 template <int DST0>
 __device__ __forceinline__ void drain_event_any(int half, float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8,
-                                                bool two, float sw0, float sw1, float sa_lo, float sa_hi) {
+                                                bool two, bool small, float sw0, float sw1, const float* sa) {
   switch (half) {
     case 8:
-      drain_event<8, DST0>(acc2, addrA, addrB, i8, two, sw0, sw1, sa_lo, sa_hi);
+      drain_event<8, DST0>(acc2, addrA, addrB, i8, two, small, sw0, sw1, sa);
       break;
     case 16:
-      drain_event<16, DST0>(acc2, addrA, addrB, i8, two, sw0, sw1, sa_lo, sa_hi);
+      drain_event<16, DST0>(acc2, addrA, addrB, i8, two, small, sw0, sw1, sa);
       break;
     case 32:
-      drain_event<32, DST0>(acc2, addrA, addrB, i8, two, sw0, sw1, sa_lo, sa_hi);
+      drain_event<32, DST0>(acc2, addrA, addrB, i8, two, small, sw0, sw1, sa);
+      break;
+    case 48:  // single mat, 96-token tile
+      if constexpr (DST0 == 0) drain_event<48, 0>(acc2, addrA, addrB, i8, false, small, sw0, sw1, sa);
       break;
     default:
-      if constexpr (DST0 == 0) drain_event<64, 0>(acc2, addrA, addrB, i8, false, sw0, sw1, sa_lo, sa_hi);
+      if constexpr (DST0 == 0) drain_event<64, 0>(acc2, addrA, addrB, i8, false, small, sw0, sw1, sa);
       break;
   }
 }
@@ -360,7 +429,7 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned l
 }
 
 struct MmaState {
-  uint32_t stage, sphase, abuf, acc_ph, ar_ph;
+  uint32_t stage, sphase, abuf, acc_ph, aidx;  // aidx: TS stages so far (A slot = aidx & 1)
 };
 
 // One sub-loop of MMAs (all K stages of one or two mats sharing the token tile), specialised on the MMA
@@ -368,19 +437,26 @@ struct MmaState {
 __device__ __forceinline__ uint32_t bcast(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
 
 // One sub-loop of MMAs (all K stages of one or two mats sharing the token tile), specialised on the MMA
-// kind and the number of mats. Executed by the whole MMA warp with warp-uniform operands (broadcast from
-// lane 0) and the tcgen05 instructions inside one elect.sync block per stage: this keeps the operands in
-// uniform registers (no per-lane "waterfall" loop around each MMA) — the issue queue is shallow, so every
-// instruction between MMAs costs tensor-core time.
-template <bool I8, bool TWO>
+// kind, the number of mats and the A-operand source (MODE 0: both A images in smem (SS); 1: all A in the
+// TMEM ring (TS); 2: per-mat at run time). Executed by the whole MMA warp with warp-uniform operands
+// (broadcast from lane 0) and the tcgen05 instructions inside one elect.sync block per stage: this keeps the
+// operands in uniform registers (no per-lane "waterfall" loop around each MMA). The issue queue is shallow,
+// so every instruction between two stages' MMAs is a tensor-core bubble: the smem descriptors are built once
+// per sub-loop and advanced by one add per MMA (start address field += 32 B >> 4 per K step).
+template <bool I8, bool TWO, int MODE>
 __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tmem, uint32_t ns, uint32_t g128,
                                             uint32_t xform, uint32_t nt, MmaState& st, unsigned long long (&pc)[16],
                                             bool prof_on) {
-  const bool nbuf2 = TWO && !g128;
   const uint32_t idesc = I8 ? idesc_s8(nt) : idesc_bf16(nt);
-  const uint32_t s_base = smem_u32(smem);
-  const bool ts0 = (xform & 1) != 0, ts1 = (xform & 2) != 0;  // transformed mats read A from TMEM
-  uint32_t b0 = 0, b1 = 0;
+  // descriptor words: lo = start>>4 | LBO 1 << 16 ; hi = SBO 1024>>4 | version 1 << 14 | SWIZZLE_128B 2 << 29
+  const uint32_t lo0 = ((smem_u32(smem) >> 4) & 0x3FFFu) | (1u << 16);
+  constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+  constexpr uint32_t kSlotLo = kSlotBytes >> 4, kTileLo = kTileBytes >> 4;
+  const bool ts0 = MODE == 1 || (MODE == 2 && (xform & 1) != 0);
+  const bool ts1 = MODE == 1 || (MODE == 2 && (xform & 2) != 0);
+  const bool any_ts = MODE == 1 || (MODE == 2 && xform != 0);
+  auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
+  uint32_t b0 = 0;
   for (uint32_t ks = 0; ks < ns; ++ks) {
     const bool ev_start = g128 || ks == 0, ev_end = g128 || ks == ns - 1;
     if (ev_start) {
@@ -388,62 +464,75 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
       twait(&ctl.acce[b0], ((st.acc_ph >> b0) & 1) ^ 1, pc[4], prof_on);
       st.acc_ph ^= 1u << b0;
       st.abuf = (st.abuf + 1) & (kAccBufs - 1);
-      if (nbuf2) {
-        b1 = st.abuf;
-        twait(&ctl.acce[b1], ((st.acc_ph >> b1) & 1) ^ 1, pc[4], prof_on);
-        st.acc_ph ^= 1u << b1;
-        st.abuf = (st.abuf + 1) & (kAccBufs - 1);
-      }
     }
     const uint32_t stage = st.stage;
-    // one wait per stage: transformed stages complete `aready` only after the transform saw `full`
-    if (xform) {
-      twait(&ctl.aready[stage], (st.ar_ph >> stage) & 1, pc[6], prof_on);
-      st.ar_ph ^= 1u << stage;
+    const uint32_t d0 = tmem + b0 * (uint32_t)kAccCols;
+    const uint32_t d1 = d0 + (uint32_t)kMat1Col;
+    const uint32_t blo = lo0 + stage * kSlotLo;
+    const uint32_t aslot = st.aidx & (kASlots - 1);
+    const uint32_t at0 = tmem + kTmemA + aslot * 64u;
+    // one wait per stage: a TS stage's A slot is ready only after the transform saw the stage's data
+    if (any_ts) {
+      twait(&ctl.aready[aslot], (st.aidx / kASlots) & 1, pc[6], prof_on);
     } else {
       twait(&ctl.full[stage], st.sphase, pc[5], prof_on);
     }
+#ifdef MXM_PROF_SUBLOOP
+    const unsigned long long t_f = prof_on ? clock64() : 0ull;
     tc_fence_after();
-    const uint32_t bb = s_base + stage * kSlotBytes;
-    const uint32_t d0 = tmem + b0 * 128u;
-    const uint32_t d1 = nbuf2 ? tmem + b1 * 128u : tmem + b0 * 128u + 64u;
-    const uint32_t acc0 = ev_start ? 0u : 1u;
-    const uint32_t as0 = bb + kTileBytes, as1 = bb + 2 * kTileBytes;   // A images (SS form)
-    const uint32_t at0 = tmem + kTmemA + stage * 64u, at1 = at0 + 32u;  // A in TMEM (TS form)
+    if (prof_on) pc[14] += clock64() - t_f;
+#else
+    tc_fence_after();
+#endif
     const unsigned long long t_iss = prof_on ? clock64() : 0ull;
     if (elect_one()) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint32_t acc = k == 0 ? acc0 : 1u;
-        const uint64_t bd = sw128_kmajor_desc(bb + k * 32);
+        const uint32_t acc = (k == 0 && ev_start) ? 0u : 1u;
+        const uint64_t bd = desc(blo + 2 * k);
         if constexpr (I8) {
-          if (ts0) mma_i8_ts(d0, at0 + k * 8, bd, idesc, acc); else mma_i8(d0, sw128_kmajor_desc(as0 + k * 32), bd, idesc, acc);
+          if (ts0) mma_i8_ts(d0, at0 + k * 8, bd, idesc, acc); else mma_i8(d0, desc(blo + kTileLo + 2 * k), bd, idesc, acc);
           if constexpr (TWO) {
-            if (ts1) mma_i8_ts(d1, at1 + k * 8, bd, idesc, acc); else mma_i8(d1, sw128_kmajor_desc(as1 + k * 32), bd, idesc, acc);
+            if (ts1) mma_i8_ts(d1, at0 + 32 + k * 8, bd, idesc, acc);
+            else mma_i8(d1, desc(blo + 2 * kTileLo + 2 * k), bd, idesc, acc);
           }
         } else {
-          if (ts0) mma_bf16_ts(d0, at0 + k * 8, bd, idesc, acc); else mma_bf16(d0, sw128_kmajor_desc(as0 + k * 32), bd, idesc, acc);
+          if (ts0) mma_bf16_ts(d0, at0 + k * 8, bd, idesc, acc);
+          else mma_bf16(d0, desc(blo + kTileLo + 2 * k), bd, idesc, acc);
           if constexpr (TWO) {
-            if (ts1) mma_bf16_ts(d1, at1 + k * 8, bd, idesc, acc); else mma_bf16(d1, sw128_kmajor_desc(as1 + k * 32), bd, idesc, acc);
+            if (ts1) mma_bf16_ts(d1, at0 + 32 + k * 8, bd, idesc, acc);
+            else mma_bf16(d1, desc(blo + 2 * kTileLo + 2 * k), bd, idesc, acc);
           }
         }
       }
       mma_commit(&ctl.empty[stage]);
-      if (ev_end) {
-        mma_commit(&ctl.accf[b0]);
-        if (nbuf2) mma_commit(&ctl.accf[b1]);
-      }
+      if (any_ts) mma_commit(&ctl.aempty[aslot]);
+      if (ev_end) mma_commit(&ctl.accf[b0]);
     }
     __syncwarp();
     if (prof_on) {
       pc[11] += clock64() - t_iss;
       pc[13] += 1;
     }
+    if (any_ts) ++st.aidx;
     if (++st.stage == kStages) {
       st.stage = 0;
       st.sphase ^= 1;
     }
   }
+}
+
+template <bool I8, bool TWO>
+__device__ __forceinline__ void mma_subloop_mode(Ctl& ctl, uint8_t* smem, uint32_t tmem, uint32_t ns, uint32_t g128,
+                                                 uint32_t xform, uint32_t nt, MmaState& st,
+                                                 unsigned long long (&pc)[16], bool prof_on) {
+  const uint32_t all = TWO ? 3u : 1u;
+  if (xform == 0)
+    mma_subloop<I8, TWO, 0>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
+  else if ((xform & all) == all)
+    mma_subloop<I8, TWO, 1>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
+  else
+    mma_subloop<I8, TWO, 2>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -460,7 +549,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&ctl.full[i], 1);
       mbar_init(&ctl.empty[i], 1);
+    }
+    for (int i = 0; i < kASlots; ++i) {
       mbar_init(&ctl.aready[i], kXfWarps);
+      mbar_init(&ctl.aempty[i], 1);
     }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&ctl.accf[i], 1);
@@ -488,6 +580,19 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   for (int i = 0; i < 16; ++i) pc[i] = 0;
   const unsigned long long t_start = clock64();
 
+  // register rebalancing from the launch-time 96 per thread: setmaxnreg.inc only draws on what .dec released,
+  // so the budget must balance exactly: 128 x (96-64) + 256 x (96-80) = 256 x (128-96)
+#ifndef MXM_REG_LO
+#define MXM_REG_LO 64
+#define MXM_REG_XF 80
+#define MXM_REG_HI 128
+#endif
+  static_assert(MXM_REG_LO == 0 || 128 * (96 - MXM_REG_LO) + 256 * (96 - MXM_REG_XF) >= 256 * (MXM_REG_HI - 96),
+                "setmaxnreg budget");
+  if (warp < 4) {
+#if MXM_REG_LO > 0
+  regs_dec<MXM_REG_LO>();
+#endif
   if (warp == 0) {
     // =========================== producer
     if (lane == 0) {
@@ -518,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           fence_proxy_async_global();
         }
         SubLoop sl[2];
-        const int nsl = build_subloops(t, p.ex, sl);
+        const int nsl = build_subloops(t, p.ex, p.d, sl);
         const int nti = nt_index(t.nt);
         for (int si = 0; si < nsl; ++si) {
           const SubLoop s = sl[si];
@@ -529,8 +634,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const uint32_t cb0 = (uint32_t)g0.code_bytes, mb0 = (uint32_t)g0.meta_bytes;
           const uint32_t cb1 = (uint32_t)g1.code_bytes, mb1 = (uint32_t)g1.meta_bytes;
           const int gst0 = g0.group / g0.ks, gst1 = g1.group / g1.ks;
-          const uint8_t* src0 = s.mat[0]->packed + (int64_t)t.ntile * g0.rb_bytes;
-          const uint8_t* src1 = s.nmats == 2 ? s.mat[1]->packed + (int64_t)t.ntile * g1.rb_bytes : nullptr;
+          const uint8_t* src0 = s.mat[0]->packed + (int64_t)s.tile[0] * g0.rb_bytes;
+          const uint8_t* src1 = s.nmats == 2 ? s.mat[1]->packed + (int64_t)s.tile[1] * g1.rb_bytes : nullptr;
           uint8_t* const dst0 = tileX(0, 0);
           uint8_t* const dst1 = tileX(0, 1);
           const int str0 = kSlotBytes, str1 = kSlotBytes;
@@ -564,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     const uint32_t tm = bcast(tmem);
     uint32_t stage = 0, sphase = 0, abuf = 0;
     uint32_t acc_ph = 0;  // bit b: parity of the next wait on acce[b] (phase bits, no local arrays)
-    uint32_t ar_ph = 0;   // bit s: parity of the next wait on aready[s]
+    uint32_t aidx = 0;    // TS stages issued so far (A-ring slot and parity)
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
       twait(&ctl.tfull[slot], rphase, pc[3], prof_on);
@@ -575,36 +680,47 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       if (phase == 255) break;
       if (phase == 1) continue;
       SubLoop sl[2];
-      const int nsl = (int)bcast((uint32_t)build_subloops(t, p.ex, sl));
+      const int nsl = (int)bcast((uint32_t)build_subloops(t, p.ex, p.d, sl));
       const uint32_t nt = bcast(t.nt);
       for (int si = 0; si < nsl; ++si) {
         const SubLoop s = sl[si];
         const uint32_t ns = bcast((uint32_t)s.ns), g128 = bcast((uint32_t)s.g128), xf = bcast((uint32_t)s.xform);
         const uint32_t i8 = bcast((uint32_t)s.i8), two = bcast((uint32_t)(s.nmats == 2));
-        MmaState st{stage, sphase, abuf, acc_ph, ar_ph};
+        MmaState st{stage, sphase, abuf, acc_ph, aidx};
+#ifdef MXM_PROF_SUBLOOP
+        const unsigned long long t_sl = prof_on ? clock64() : 0ull;
+#endif
         if (i8) {
           if (two)
-            mma_subloop<true, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+            mma_subloop_mode<true, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
           else
-            mma_subloop<true, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+            mma_subloop_mode<true, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
         } else {
           if (two)
-            mma_subloop<false, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+            mma_subloop_mode<false, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
           else
-            mma_subloop<false, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+            mma_subloop_mode<false, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
         }
+#ifdef MXM_PROF_SUBLOOP
+        if (prof_on) pc[12] += clock64() - t_sl;
+#endif
         stage = st.stage;
         sphase = st.sphase;
         abuf = st.abuf;
         acc_ph = st.acc_ph;
-        ar_ph = st.ar_ph;
+        aidx = st.aidx;
       }
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < 8) {
-    // =========================== transform warpgroup: one A row per thread, both mats of the stage
-    const int r = threadIdx.x - 128;
-    uint32_t stage = 0, sphase = 0;
+  }
+  } else if ((warp >= 4 && warp < 8) || warp >= 16) {
+    // =========================== transform: two warpgroups, each one K half of every stage, one A row per thread
+#if MXM_REG_LO > 0
+    regs_dec<MXM_REG_XF>();
+#endif
+    const int r = threadIdx.x & 127;
+    const int xh = warp >= 16;
+    uint32_t stage = 0, sphase = 0, aidx = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
       twait(&ctl.tfull[slot], rphase, pc[7], prof_on);
@@ -614,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       if (t.phase == 255) break;
       if (t.phase == 1) continue;
       SubLoop sl[2];
-      const int nsl = build_subloops(t, p.ex, sl);
+      const int nsl = build_subloops(t, p.ex, p.d, sl);
       for (int si = 0; si < nsl; ++si) {
         const SubLoop s = sl[si];
         const bool two = s.nmats == 2;
@@ -634,32 +750,33 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           if (++gca == gstA) gca = 0;
           if (++gcb == gstB) gcb = 0;
           if (s.xform) {
+            const uint32_t aslot = aidx & (kASlots - 1);
+            twait(&ctl.aempty[aslot], ((aidx / kASlots) & 1) ^ 1, pc[8], prof_on);  // MMA done with the slot
             twait(&ctl.full[stage], sphase, pc[8], prof_on);
-            // dequantized / unpacked rows go to the TMEM A ring (lane = row); one tcgen05.st per mat
-            const uint32_t tA = tmem + ((uint32_t)(r & ~31) << 16) + kTmemA + stage * 64u;
-            uint32_t o[32];
-            if (s.i8) {
-              if (xa) {
-                if (bitsA == 4) xform_wa<4>(tileX(stage, 0), r, o); else xform_wa<5>(tileX(stage, 0), r, o);
-                tmem_st32(tA, o);
-              }
-              if (xb) {
-                if (bitsB == 4) xform_wa<4>(tileX(stage, 1), r, o); else xform_wa<5>(tileX(stage, 1), r, o);
-                tmem_st32(tA + 32, o);
-              }
-            } else {
-              if (xa) {
-                xform_wo_any(bitsA, tileX(stage, 0), hmA, mbA, symA, offA, r, sa, za, o);
-                tmem_st32(tA, o);
-              }
-              if (xb) {
-                xform_wo_any(bitsB, tileX(stage, 1), hmB, mbB, symB, offB, r, sb, zb, o);
-                tmem_st32(tA + 32, o);
-              }
+            tc_fence_after();
+            // dequantized / unpacked rows go to the TMEM A ring (lane = row); one tcgen05.st per mat and K half
+            const uint32_t tA = tmem + ((uint32_t)(r & ~31) << 16) + kTmemA + aslot * 64u;
+#ifdef MXM_ABL_XFORM
+            {
+              uint32_t oz[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) oz[i] = 0x3f803f80u;
+              tmem_st16(tA + 16 * xh, oz);
+              if (s.nmats == 2) tmem_st16(tA + 32 + 16 * xh, oz);
             }
+            if (0)
+#endif
+            if (xh)
+              xform_stage<1>(s, tileX(stage, 0), tileX(stage, 1), tA, r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
+                             offA, offB, xa, xb, sa, za, sb, zb);
+            else
+              xform_stage<0>(s, tileX(stage, 0), tileX(stage, 1), tA, r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
+                             offA, offB, xa, xb, sa, za, sb, zb);
             tmem_st_wait();
+            tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&ctl.aready[stage]);
+            if (lane == 0) mbar_arrive(&ctl.aready[aslot]);
+            ++aidx;
           }
           if (++stage == kStages) {
             stage = 0;
@@ -668,8 +785,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && warp < 16) {
     // =========================== epilogue (2 warpgroups)
+#if MXM_REG_LO > 0
+    regs_inc<MXM_REG_HI>();
+#endif
     const int ew = warp - 8, wg = ew >> 2, q = warp & 3;
     const int l = q * 32 + lane;  // output channel within the tile == TMEM lane
     uint32_t abuf = 0, acc_ph = 0, rbuf = 0;
@@ -728,11 +848,12 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         continue;
       }
       SubLoop sl[2];
-      const int nsl = build_subloops(t, p.ex, sl);
+      const int nsl = build_subloops(t, p.ex, p.d, sl);
       const bool reg_mode = nsl == 2 || sl[0].g128;
       const int half = t.nt >> 1;
       const int col0 = wg * half;
-      const int n = t.ntile * 128 + l;
+      const int n = sl[0].tile[0] * 128 + l;                       // mat 0's output channel
+      const int n1 = sl[0].tile[nsl == 1 ? 1 : 0] * 128 + l;       // mat 1's (paired down tiles)
       const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
       float2 acc2[32];
 #pragma unroll
@@ -745,7 +866,6 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       for (int si = 0; si < nsl; ++si) {
         const SubLoop s = sl[si];
         const bool two = s.nmats == 2;
-        const bool nbuf2 = two && !s.g128;
         const int nev = s.g128 ? s.ns : 1;
         const float* xs_s = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;
         const uint16_t* wsc0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off);
@@ -765,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         float nsw0 = 1.f, nsw1 = 1.f, nsa_lo = 1.f, nsa_hi = 1.f;
         if (s.i8 && pre) {
           nsw0 = bf16f(__ldg(wsc0 + n));
-          if (two) nsw1 = bf16f(__ldg(wsc1 + n));
+          if (two) nsw1 = bf16f(__ldg(wsc1 + n1));
           nsa_lo = vlo ? __ldg(xs_lo) : 0.f;
           nsa_hi = vhi ? __ldg(xs_hi) : 0.f;
         }
@@ -773,33 +893,29 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           float sw0 = nsw0, sw1 = nsw1, sa_lo = nsa_lo, sa_hi = nsa_hi;
           const uint32_t b0 = abuf;
           abuf = (abuf + 1) & (kAccBufs - 1);
-          uint32_t b1 = b0;
-          if (nbuf2) {
-            b1 = abuf;
-            abuf = (abuf + 1) & (kAccBufs - 1);
-          }
           twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
           acc_ph ^= 1u << b0;
-          if (nbuf2) {
-            twait(&ctl.accf[b1], (acc_ph >> b1) & 1, pc[10], prof_on);
-            acc_ph ^= 1u << b1;
-          }
           tc_fence_after();
           if (s.i8 && !pre) {
             sw0 = bf16f(__ldg(wsc0 + (int64_t)ev * wN + n));
-            if (two) sw1 = bf16f(__ldg(wsc1 + (int64_t)ev * wN + n));
+            if (two) sw1 = bf16f(__ldg(wsc1 + (int64_t)ev * wN + n1));
             sa_lo = vlo ? __ldcg(xs_lo + ev) : 0.f;
             sa_hi = vhi ? __ldcg(xs_hi + ev) : 0.f;
           }
           if (s.i8 && pre && ev + 1 < nev) {
             nsw0 = bf16f(__ldg(wsc0 + (int64_t)(ev + 1) * wN + n));
-            if (two) nsw1 = bf16f(__ldg(wsc1 + (int64_t)(ev + 1) * wN + n));
+            if (two) nsw1 = bf16f(__ldg(wsc1 + (int64_t)(ev + 1) * wN + n1));
             nsa_lo = vlo ? __ldg(xs_lo + ev + 1) : 0.f;
             nsa_hi = vhi ? __ldg(xs_hi + ev + 1) : 0.f;
           }
-          const uint32_t colA = b0 * 128u;
-          const uint32_t colB = nbuf2 ? b1 * 128u : b0 * 128u + 64u;
+          const uint32_t colA = b0 * (uint32_t)kAccCols;
+          const uint32_t colB = colA + (uint32_t)kMat1Col;
+#ifdef MXM_ABL_EPI
+          if (true) {
+          } else if (!reg_mode) {
+#else
           if (!reg_mode) {
+#endif
             // ---- streaming epilogue: one drain event for the whole task
             float rw_lo = 0.f, rw_hi = 0.f;
             if (t.phase == 2) {
@@ -840,6 +956,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
                     const int64_t row = (int64_t)t.row0 + col;
                     const float o = s.i8 ? (float)(int32_t)va[j] * (sw0 * sa) : __uint_as_float(va[j]);
                     p.O[row * p.d + n] = f2bf(o * rw);
+                    if (two) {
+                      const float o1 = s.i8 ? (float)(int32_t)vb[j] * (sw1 * sa) : __uint_as_float(vb[j]);
+                      p.O[row * p.d + n1] = f2bf(o1 * rw);
+                    }
                   }
                 }
               }
@@ -848,17 +968,21 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             // ---- register-accumulating epilogue (g128 drains / hetero gate-up)
             const bool dst_hi = t.phase == 0 && nsl == 2 && si == 1;  // hetero: the up sub-loop
             const uint32_t aA = lane_addr + colA + (uint32_t)col0, aB = lane_addr + colB + (uint32_t)col0;
+            float* sa_w = ctl.sa[ew];
+            if (s.i8) {
+              __syncwarp();  // previous event's broadcast reads are done
+              sa_w[lane] = sa_lo;
+              sa_w[32 + lane] = sa_hi;
+              __syncwarp();
+            }
             if (dst_hi)
-              drain_event_any<16>(half, acc2, aA, aB, s.i8, false, sw0, sw1, sa_lo, sa_hi);
+              drain_event_any<16>(half, acc2, aA, aB, s.i8, false, s.g128, sw0, sw1, sa_w);
             else
-              drain_event_any<0>(half, acc2, aA, aB, s.i8, two, sw0, sw1, sa_lo, sa_hi);
+              drain_event_any<0>(half, acc2, aA, aB, s.i8, two, s.g128, sw0, sw1, sa_w);
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&ctl.acce[b0]);
-            if (nbuf2) mbar_arrive(&ctl.acce[b1]);
-          }
+          if (lane == 0) mbar_arrive(&ctl.acce[b0]);
         }
       }
       if (reg_mode) {
@@ -878,12 +1002,14 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const int cl = col0 + lane, ch = col0 + 32 + lane;
           rw_lo = (lane < half && cl < t.rows) ? __ldg(p.row_w + t.row0 + cl) : 0.f;
           rw_hi = (32 + lane < half && ch < t.rows) ? __ldg(p.row_w + t.row0 + ch) : 0.f;
-#pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            if (c < half) {
-              const int col = col0 + c;
-              const float rw = colval(rw_lo, rw_hi, c);
-              if (col < t.rows) p.O[((int64_t)t.row0 + col) * p.d + n] = f2bf(acc[c] * rw);
+          const bool two = sl[0].nmats == 2;  // paired down tiles: mat 1 in acc[32..63]
+#pragma unroll 1
+          for (int c = 0; c < half; ++c) {
+            const int col = col0 + c;
+            const float rw = colval(rw_lo, rw_hi, c);
+            if (col < t.rows) {
+              p.O[((int64_t)t.row0 + col) * p.d + n] = f2bf(acc[c] * rw);
+              if (two) p.O[((int64_t)t.row0 + col) * p.d + n1] = f2bf(acc[32 + c] * rw);
             }
           }
         }

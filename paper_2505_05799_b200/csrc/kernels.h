@@ -9,7 +9,7 @@
 namespace mxm {
 
 struct GemmParams {
-  CUtensorMap tmap[5][4];  // B sources {Xb, XqA, XqB, H, Hq} x token tile {16, 32, 64, 128}
+  CUtensorMap tmap[5][4];  // B sources {Xb, XqA, XqB, H, Hq} x token tile {16, 32, 64, 96}
   const ExpertDesc* ex;
   const Task* tasks;
   int32_t* meta;  // [0] n_tasks, [5] queue head, [6] executed tasks

@@ -4,8 +4,8 @@
 // SMs and its scheduler "prioritizes computationally intensive tiles" (greedy makespan,
 // P:231; Graham's bound). Here: every (expert, m-tile) group contributes f/128 gate+up tiles
 // (phase 1), ceil(rows/32) h-quantization sub-tasks when its down block is weight-activation, and
-// d/128 down tiles (phase 2). Groups are ordered by estimated per-tile cost, descending (LPT);
-// the whole phase-1 list precedes the h-quant list which precedes phase 2, so the dynamic queue
+// its down tasks (phase 2): pairs of 128-channel tiles (down_pair, common.cuh) or single tiles.
+// Groups are ordered by estimated per-tile cost, descending (LPT); the whole phase-1 list precedes the h-quant list which precedes phase 2, so the dynamic queue
 // of the persistent kernel can never deadlock on a dependency.
 #include <cstdint>
 
@@ -45,8 +45,9 @@ __device__ int block_excl_scan(int v, int* warp_tot, int* out_total) {
   return base + x - v;
 }
 
+// token tile of an m-tile with m rows: 16 / 32 / 64 / 96 (the TMA boxes, MMA N)
 __device__ __forceinline__ int pow2_tile(int m) {
-  return m <= 16 ? 16 : (m <= 32 ? 32 : (m <= 64 ? 64 : 128));
+  return m <= 16 ? 16 : (m <= 32 ? 32 : (m <= 64 ? 64 : 96));
 }
 
 __device__ __forceinline__ float tile_cost(const ExpertDesc& e, int d, int nt) {
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
   __shared__ float s_cf[kMaxV], s_cr[kMaxV];
   __shared__ int s_order[kMaxV];
   __shared__ int s_G, s_full;
+  int32_t* grp_n2 = hq_done;  // per-group down-task count (scratch: hq_done is zeroed after the scan)
   const int tid = threadIdx.x;
   if (tid < V) {
     const ExpertDesc& e = ex[tid];
@@ -77,8 +79,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
       cnt = ((tid + 1 < E) ? v_off[tid + 1] : v_off[V]) - v_off[tid];
     else
       cnt = (int)T;
-    const bool reg_dual = !e.dual || (kind_is_i8(e.blk[0].geo.kind) && e.blk[0].geo.group == 128);
-    const int cap = reg_dual ? 64 : 128;
+    const int cap = tile_cap(e);
     int nfull = 0, rem = 0;
     if (cnt > cap) {
       nfull = cnt / cap;
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
       grp_nt[g] = s_cap[v];
       grp_n1[g] = e.inter / 128;
       grp_nq[g] = wa_down ? (s_cap[v] + 31) / 32 : 0;
+      grp_n2[g] = down_tasks(e, s_cap[v], d / 128);
     }
     if (s_rem[v] > 0) {
       const int g = s_ragid[v];
@@ -159,13 +161,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
       grp_nt[g] = pow2_tile(s_rem[v]);
       grp_n1[g] = e.inter / 128;
       grp_nq[g] = wa_down ? (s_rem[v] + 31) / 32 : 0;
+      grp_n2[g] = down_tasks(e, pow2_tile(s_rem[v]), d / 128);
     }
   }
   __syncthreads();
-  for (int g = tid; g < G; g += kPlanThreads) {
-    p1_done[g] = 0;
-    hq_done[g] = 0;
-  }
+  for (int g = tid; g < G; g += kPlanThreads) p1_done[g] = 0;
   // prefix sums of per-group task counts (3 phases); each thread owns a contiguous gid range
   const int per = (G + kPlanThreads - 1) / kPlanThreads;
   const int g0 = min(G, tid * per), g1 = min(G, g0 + per);
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
   for (int g = g0; g < g1; ++g) {
     c1 += grp_n1[g];
     cq += grp_nq[g];
-    c2 += d / 128;
+    c2 += grp_n2[g];
   }
   __shared__ int s_wt[32];
   int t1, tq, t2;
@@ -210,11 +210,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
       tasks[oq++] = t;
     }
     t.phase = 2;
-    for (int j = 0; j < d / 128; ++j) {
-      t.ntile = (uint16_t)j;
+    for (int j = 0; j < grp_n2[g]; ++j) {
+      t.ntile = (uint16_t)j;  // down tile (or tile pair) index
       tasks[o2++] = t;
     }
   }
+  __syncthreads();  // every thread has read its grp_n2 entries before the scratch is cleared
+  for (int g = tid; g < G; g += kPlanThreads) hq_done[g] = 0;
 }
 
 cudaError_t launch_plan(const ExpertDesc* ex, int V, int E, int64_t T, int d, const int32_t* v_off, int g_max,

@@ -7,8 +7,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py --config $CFG ${BENCH_ARGS} > gpurun_out/bench_$CFG.json 2> gpurun_out/bench_$CFG.err; echo "bench rc=$?"
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_$CFG.csv \
-     python bench.py --config $CFG --steps 3 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>gpurun_out/ncu1.err
+     python bench.py --config $CFG --steps 3 --warmup 1 --no-cpu-baseline --no-e2e --no-comparators > /dev/null 2>gpurun_out/ncu1.err
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:moe_gemm -s 1 -c 1 -o gpurun_out/prof_$CFG -f \
-     python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>gpurun_out/ncu2.err
+     python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-comparators > /dev/null 2>gpurun_out/ncu2.err
 fi
 cat gpurun_out/i8.log gpurun_out/smoke.log; tail -3 gpurun_out/bench_$CFG.err; cat gpurun_out/bench_$CFG.json
