@@ -145,7 +145,8 @@ mxm_status mxm_layer_profile_read(mxm_layer* l, float* ms, int32_t n, int32_t* n
  * (uint64 [num_SMs][16], caller-zeroed; NULL disables). Slots: 0 producer ring-slot wait, 1 producer
  * stage-free wait, 2 producer dependency wait, 3-6 MMA waits (task, accumulator, data, transform),
  * 7-8 transform waits (task, data), 9-10 epilogue waits (task, accumulator), 13 MMA stages issued,
- * 14 h-quant dependency wait, 15 kernel cycles. */
+ * 14 h-quant dependency wait, 15 kernel cycles. Only a library built with -DMXM_DEBUG_COUNTERS records
+ * them (the product build compiles the counters out); otherwise a non-NULL dev_buf is MXM_E_CONFIG. */
 mxm_status mxm_layer_debug_counters(mxm_layer* l, void* dev_buf);
 /* Number of library kernels one mxm_moe_group_gemm call launches (route x3-4, gather, plan, GEMM, combine). */
 int32_t mxm_kernels_per_call(const mxm_layer* l);

@@ -386,6 +386,7 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   prm.H = (uint16_t*)P(w.H);
   prm.Hq = (int8_t*)P(w.Hq);
   prm.Hs = (float*)P(w.Hs);
+  prm.hs_stride = w.R;
   prm.hmax = (uint32_t*)P(w.hmax);
   prm.O = (uint16_t*)P(w.O);
   prm.row_w = row_w;
@@ -427,6 +428,9 @@ mxm_status mxm_layer_profile_read(mxm_layer* l, float* ms, int32_t n, int32_t* n
 
 mxm_status mxm_layer_debug_counters(mxm_layer* l, void* dev_buf) {
   if (!l) return fail(MXM_E_CONFIG, "null layer");
+#ifndef MXM_DEBUG_COUNTERS
+  if (dev_buf) return fail(MXM_E_CONFIG, "library built without MXM_DEBUG_COUNTERS (see tools/diag_waits.py)");
+#endif
   l->prof_counters = dev_buf;
   return MXM_OK;
 }

@@ -44,7 +44,7 @@ constexpr int kTileBytes = 16384;
 constexpr int kSlotBytes = 3 * kTileBytes;  // per stage: token tile B | mat 0 (raw codes or A image) | mat 1
 
 constexpr int kOffCtl = kStages * kSlotBytes;
-constexpr int kCtlBytes = 4096;
+constexpr int kCtlBytes = 8192;
 constexpr int kSmemBytes = kOffCtl + kCtlBytes + 1024;
 
 struct Ctl {
@@ -55,7 +55,8 @@ struct Ctl {
   Task ring[kRing];
   uint32_t tmem_base;
   uint32_t colmax[2][2][4][8];  // [buffer][warpgroup][lane quarter][column] for the fused g128 h-quant
-  alignas(16) float sa[8][64];  // per epilogue warp: activation scales of the current drain event
+  alignas(16) float cw[8][2][64];  // per epilogue warp: [0] activation scale of the current drain event,
+                                   // [1] route weight of this warp's token columns (broadcast reads)
 };
 static_assert(sizeof(Ctl) <= kCtlBytes, "ctl");
 
@@ -367,52 +368,54 @@ __device__ __forceinline__ void drain_event_any(int half, float2 (&acc2)[32], ui
   }
 }
 
-// h for 8 token columns [colc, colc+8) of output channel n (= this thread's TMEM lane) in the form the
-// down block consumes (dmode): 0 bf16 H (weight-only / bf16 down); 1 bf16 H + row max|h| via atomicMax
-// (per-token W-A down, quantized later in one pass); 2 fused per-128-group quantization: the group is
-// exactly this tile's 128 channels, so codes + scale are produced here (DESIGN R9).
-__device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int dmode, int qmax, int n, int colc,
-                                        const float (&h)[8], Ctl& ctl, int wg, int q, int lane, uint32_t& rbuf) {
-  float hf[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) hf[j] = bf16f(f2bf(h[j]));  // h is defined in bf16 (DESIGN R16)
+// h for 8 token columns [colc, colc+8) of output channel n (= this thread's TMEM lane), already rounded to
+// bf16 (hb, DESIGN R16), in the form the down block consumes (dmode): 0 bf16 H; 1 bf16 H + row max|h| via
+// atomicMax (per-token W-A down, quantized later in one pass); 2 fused per-128-group quantization: the group
+// is exactly this tile's 128 channels, so codes + scale are produced here (DESIGN R9).
+// nv = valid columns from colc (rows of the m-tile), hrow = &H[row0 + colc][n] (row stride f_max).
+__device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int dmode, int qmax, int n, int colc, int nv,
+                                     const uint16_t (&hb)[8], Ctl& ctl, int wg, int q, int lane, uint32_t& rbuf) {
+  const int64_t row0 = (int64_t)t.row0 + colc;
   if (dmode == 2) {
     uint32_t m[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) m[j] = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(hf[j])));
+    for (int j = 0; j < 8; ++j) m[j] = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(bf16f(hb[j]))));
     if (lane == 0)
 #pragma unroll
       for (int j = 0; j < 8; ++j) ctl.colmax[rbuf][wg][q][j] = m[j];
     named_bar_sync(2 + wg, 128);
+    // lanes 0..7 derive column (lane)'s reciprocal / scale once (IEEE division, DESIGN R9), then broadcast
+    const float fq = (float)qmax;
+    float r_l = 0.f, sc_l = 1.f;
+    if (lane < 8) {
+      const uint32_t a = max(max(ctl.colmax[rbuf][wg][0][lane], ctl.colmax[rbuf][wg][1][lane]),
+                             max(ctl.colmax[rbuf][wg][2][lane], ctl.colmax[rbuf][wg][3][lane]));
+      const float amax = __uint_as_float(a);
+      if (amax > 0.f) {
+        r_l = __fdiv_rn(fq, amax);
+        sc_l = __fdiv_rn(amax, fq);
+      }
+      if (q == 0 && lane < nv) p.Hs[row0 + lane + (int64_t)t.ntile * p.hs_stride] = sc_l;
+    }
+    int8_t* hq = p.Hq + row0 * p.f_max + n;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const uint32_t a = max(max(ctl.colmax[rbuf][wg][0][j], ctl.colmax[rbuf][wg][1][j]),
-                             max(ctl.colmax[rbuf][wg][2][j], ctl.colmax[rbuf][wg][3][j]));
-      const float amax = __uint_as_float(a), fq = (float)qmax;
-      const float r = amax > 0.f ? __fdiv_rn(fq, amax) : 0.f;
-      const float sc = amax > 0.f ? __fdiv_rn(amax, fq) : 1.f;
-      const int col = colc + j;
-      if (col < t.rows) {
-        const int64_t row = (int64_t)t.row0 + col;
-        const float qv = fminf(fmaxf(rintf(__fmul_rn(hf[j], r)), -fq), fq);
-        p.Hq[row * p.f_max + n] = (int8_t)(int)qv;
-        if (q == 0 && lane == 0) p.Hs[row * (p.f_max / 128) + t.ntile] = sc;
-      }
+      const float r = __shfl_sync(0xffffffffu, r_l, j);
+      const float qv = fminf(fmaxf(rintf(__fmul_rn(bf16f(hb[j]), r)), -fq), fq);
+      if (j < nv) hq[(int64_t)j * p.f_max] = (int8_t)(int)qv;
     }
     rbuf ^= 1;
     return;
   }
+  uint16_t* hrow = p.H + row0 * p.f_max + n;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int col = colc + j;
-    if (col < t.rows) p.H[((int64_t)t.row0 + col) * p.f_max + n] = f2bf(hf[j]);
-  }
+  for (int j = 0; j < 8; ++j)
+    if (j < nv) hrow[(int64_t)j * p.f_max] = hb[j];
   if (dmode == 1) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(hf[j])));
-      const int col = colc + j;
-      if (lane == 0 && col < t.rows) atomicMax(p.hmax + t.row0 + col, m);
+      const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(bf16f(hb[j]))));
+      if (lane == 0 && j < nv) atomicMax(p.hmax + row0 + j, m);
     }
   }
 }
@@ -477,7 +480,7 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
     } else {
       twait(&ctl.full[stage], st.sphase, pc[5], prof_on);
     }
-#ifdef MXM_PROF_SUBLOOP
+#if defined(MXM_PROF_SUBLOOP) && defined(MXM_DEBUG_COUNTERS)
     const unsigned long long t_f = prof_on ? clock64() : 0ull;
     tc_fence_after();
     if (prof_on) pc[14] += clock64() - t_f;
@@ -574,7 +577,13 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = ctl.tmem_base;
   const int n_tasks = p.meta[0];
+  // wait-site cycle counters: compiled in only for the diagnostic build (tools/diag_waits.py); in the
+  // product build they fold away (they would otherwise pin 32 registers in every role)
+#ifdef MXM_DEBUG_COUNTERS
   const bool prof_on = p.prof != nullptr;
+#else
+  constexpr bool prof_on = false;
+#endif
   unsigned long long pc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) pc[i] = 0;
@@ -687,7 +696,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         const uint32_t ns = bcast((uint32_t)s.ns), g128 = bcast((uint32_t)s.g128), xf = bcast((uint32_t)s.xform);
         const uint32_t i8 = bcast((uint32_t)s.i8), two = bcast((uint32_t)(s.nmats == 2));
         MmaState st{stage, sphase, abuf, acc_ph, aidx};
-#ifdef MXM_PROF_SUBLOOP
+#if defined(MXM_PROF_SUBLOOP) && defined(MXM_DEBUG_COUNTERS)
         const unsigned long long t_sl = prof_on ? clock64() : 0ull;
 #endif
         if (i8) {
@@ -701,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           else
             mma_subloop_mode<false, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
         }
-#ifdef MXM_PROF_SUBLOOP
+#if defined(MXM_PROF_SUBLOOP) && defined(MXM_DEBUG_COUNTERS)
         if (prof_on) pc[12] += clock64() - t_sl;
 #endif
         stage = st.stage;
@@ -837,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             }
             dst[i] = make_uint2(o[0], o[1]);
           }
-          if (lane == 0) p.Hs[row * (p.f_max / 128)] = sc;
+          if (lane == 0) p.Hs[row] = sc;  // per-token: group 0 of the group-major [g][R] layout
         }
         named_bar_sync(1, 256);
         if (ew == 0 && lane == 0) {
@@ -852,164 +861,204 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       const bool reg_mode = nsl == 2 || sl[0].g128;
       const int half = t.nt >> 1;
       const int col0 = wg * half;
-      const int n = sl[0].tile[0] * 128 + l;                       // mat 0's output channel
-      const int n1 = sl[0].tile[nsl == 1 ? 1 : 0] * 128 + l;       // mat 1's (paired down tiles)
+      const int nvalid = t.rows - col0;                          // columns of this warpgroup with a real row
+      const int n = sl[0].tile[0] * 128 + l;                     // mat 0's output channel
+      const int n1 = sl[0].tile[nsl == 1 ? 1 : 0] * 128 + l;     // mat 1's (paired down tiles)
       const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
-      float2 acc2[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc2[i] = make_float2(0.f, 0.f);
-      const int xs_stride = t.phase == 0 ? p.d / 128 : p.f_max / 128;
+      float* cw_sa = ctl.cw[ew][0];
+      float* cw_rw = ctl.cw[ew][1];
+      const int cl = col0 + lane, ch = col0 + 32 + lane;
+      const bool vlo = lane < half && cl < t.rows, vhi = 32 + lane < half && ch < t.rows;
+      if (t.phase == 2) {  // route weights of this warp's columns, read back as broadcast float4s
+        __syncwarp();
+        cw_rw[lane] = vlo ? __ldg(p.row_w + t.row0 + cl) : 0.f;
+        cw_rw[32 + lane] = vhi ? __ldg(p.row_w + t.row0 + ch) : 0.f;
+        __syncwarp();
+      }
       const LinDesc& Ld = E.blk[2];
       const int dmode = !kind_is_i8(Ld.geo.kind) ? 0 : (Ld.geo.group == 128 ? 2 : 1);
       const int dqmax = (1 << (Ld.a_bits - 1)) - 1;
-
-      for (int si = 0; si < nsl; ++si) {
-        const SubLoop s = sl[si];
+      if (!reg_mode) {
+        // ======== streaming epilogue: one drain event for the whole task (dual phase 0, or phase 2)
+        const SubLoop s = sl[0];
         const bool two = s.nmats == 2;
-        const int nev = s.g128 ? s.ns : 1;
-        const float* xs_s = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;
-        const uint16_t* wsc0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off);
-        const uint16_t* wsc1 =
-            two ? reinterpret_cast<const uint16_t*>(s.mat[1]->packed + s.mat[1]->geo.wa_scale_off) : wsc0;
-        const int64_t wN = s.mat[0]->geo.N;
-        // per-group scales of event ev (weight s_w[n, g] per thread, activation s_a[row, g] per lane-column),
-        // prefetched one event ahead so their load latency overlaps the previous drain / the MMA wait
-        const int cl = col0 + lane, ch = col0 + 32 + lane;
-        const bool vlo = lane < half && cl < t.rows, vhi = 32 + lane < half && ch < t.rows;
-        const float* xs_lo = xs_s + ((int64_t)t.row0 + cl) * xs_stride;
-        const float* xs_hi = xs_s + ((int64_t)t.row0 + ch) * xs_stride;
-        // phase 0 reads x-scales written before this kernel (read-only path, prefetched before the wait);
-        // phase 2 reads h-scales written by this kernel: only after the first accumulator wait (the MMA has
-        // then consumed Hq, so the producer's dependency wait has passed) and through L2 (ld.cg)
-        const bool pre = t.phase == 0;
-        float nsw0 = 1.f, nsw1 = 1.f, nsa_lo = 1.f, nsa_hi = 1.f;
-        if (s.i8 && pre) {
-          nsw0 = bf16f(__ldg(wsc0 + n));
-          if (two) nsw1 = bf16f(__ldg(wsc1 + n1));
-          nsa_lo = vlo ? __ldg(xs_lo) : 0.f;
-          nsa_hi = vhi ? __ldg(xs_hi) : 0.f;
+        const float* xs_s = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;  // group-major [g][R]
+        float sw0 = 1.f, sw1 = 1.f, sa_lo = 1.f, sa_hi = 1.f;
+        if (s.i8 && t.phase == 0) {  // x-scales / weight scales exist before this kernel: load before the wait
+          const uint16_t* wsc0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off);
+          const uint16_t* wsc1 = reinterpret_cast<const uint16_t*>(s.mat[s.nmats - 1]->packed +
+                                                                  s.mat[s.nmats - 1]->geo.wa_scale_off);
+          sw0 = bf16f(__ldg(wsc0 + n));
+          sw1 = bf16f(__ldg(wsc1 + n1));
+          sa_lo = vlo ? __ldg(xs_s + (int64_t)t.row0 + cl) : 0.f;
+          sa_hi = vhi ? __ldg(xs_s + (int64_t)t.row0 + ch) : 0.f;
         }
-        for (int ev = 0; ev < nev; ++ev) {
-          float sw0 = nsw0, sw1 = nsw1, sa_lo = nsa_lo, sa_hi = nsa_hi;
-          const uint32_t b0 = abuf;
-          abuf = (abuf + 1) & (kAccBufs - 1);
-          twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
-          acc_ph ^= 1u << b0;
-          tc_fence_after();
-          if (s.i8 && !pre) {
-            sw0 = bf16f(__ldg(wsc0 + (int64_t)ev * wN + n));
-            if (two) sw1 = bf16f(__ldg(wsc1 + (int64_t)ev * wN + n1));
-            sa_lo = vlo ? __ldcg(xs_lo + ev) : 0.f;
-            sa_hi = vhi ? __ldcg(xs_hi + ev) : 0.f;
-          }
-          if (s.i8 && pre && ev + 1 < nev) {
-            nsw0 = bf16f(__ldg(wsc0 + (int64_t)(ev + 1) * wN + n));
-            if (two) nsw1 = bf16f(__ldg(wsc1 + (int64_t)(ev + 1) * wN + n1));
-            nsa_lo = vlo ? __ldg(xs_lo + ev + 1) : 0.f;
-            nsa_hi = vhi ? __ldg(xs_hi + ev + 1) : 0.f;
-          }
-          const uint32_t colA = b0 * (uint32_t)kAccCols;
-          const uint32_t colB = colA + (uint32_t)kMat1Col;
-#ifdef MXM_ABL_EPI
-          if (true) {
-          } else if (!reg_mode) {
-#else
-          if (!reg_mode) {
-#endif
-            // ---- streaming epilogue: one drain event for the whole task
-            float rw_lo = 0.f, rw_hi = 0.f;
-            if (t.phase == 2) {
-              const int cl = col0 + lane, ch = col0 + 32 + lane;
-              rw_lo = (lane < half && cl < t.rows) ? __ldg(p.row_w + t.row0 + cl) : 0.f;
-              rw_hi = (32 + lane < half && ch < t.rows) ? __ldg(p.row_w + t.row0 + ch) : 0.f;
-            }
+        const uint32_t b0 = abuf;
+        abuf = (abuf + 1) & (kAccBufs - 1);
+        twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
+        acc_ph ^= 1u << b0;
+        tc_fence_after();
+        if (s.i8 && t.phase != 0) {  // h-scales are written by this kernel: read after the MMA consumed Hq
+          const uint16_t* wsc0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off);
+          sw0 = bf16f(__ldg(wsc0 + n));
+          sw1 = bf16f(__ldg(wsc0 + n1));
+          sa_lo = vlo ? __ldcg(xs_s + (int64_t)t.row0 + cl) : 0.f;
+          sa_hi = vhi ? __ldcg(xs_s + (int64_t)t.row0 + ch) : 0.f;
+        }
+        if (s.i8) {
+          __syncwarp();
+          cw_sa[lane] = sa_lo;
+          cw_sa[32 + lane] = sa_hi;
+          __syncwarp();
+        }
+        const uint32_t colA = b0 * (uint32_t)kAccCols;
+        const uint32_t colB = colA + (uint32_t)kMat1Col;
+        const float2 swa = make_float2(sw0, sw0), swb = make_float2(sw1, sw1);
+#ifndef MXM_ABL_EPI
 #pragma unroll 1
-            for (int c = 0; c < half; c += 8) {
-              uint32_t va[8], vb[8];
-              const uint32_t cbase = (uint32_t)(col0 + c);
-              tmem_ld8(lane_addr + colA + cbase, va);
-              if (two) tmem_ld8(lane_addr + colB + cbase, vb);
-              tmem_ld_wait();
-              if (t.phase == 0) {
-                float h[8];
+        for (int c = 0; c < half; c += 8) {
+          uint32_t va[8], vb[8];
+          const uint32_t cbase = (uint32_t)(col0 + c);
+          tmem_ld8(lane_addr + colA + cbase, va);
+          if (two) tmem_ld8(lane_addr + colB + cbase, vb);
+          tmem_ld_wait();
+          float fa[8], fb[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  const float sa = colval(sa_lo, sa_hi, c + j);
-                  float g, u;
-                  if (s.i8) {
-                    g = (float)(int32_t)va[j] * (sw0 * sa);
-                    u = (float)(int32_t)vb[j] * (sw1 * sa);
-                  } else {
-                    g = __uint_as_float(va[j]);
-                    u = __uint_as_float(vb[j]);
-                  }
-                  h[j] = silu_f(g) * u;
-                }
-                emit_h8(p, t, dmode, dqmax, n, col0 + c, h, ctl, wg, q, lane, rbuf);
-              } else {
+          for (int j = 0; j < 8; ++j) {
+            fa[j] = __uint_as_float(va[j]);
+            fb[j] = __uint_as_float(vb[j]);
+          }
+          if (s.i8) {  // per-column activation scale: broadcast smem reads
+            const float4 x0 = *reinterpret_cast<const float4*>(cw_sa + c);
+            const float4 x1 = *reinterpret_cast<const float4*>(cw_sa + c + 4);
+            const float2 s2[4] = {make_float2(x0.x, x0.y), make_float2(x0.z, x0.w), make_float2(x1.x, x1.y),
+                                  make_float2(x1.z, x1.w)};
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  const int col = col0 + c + j;
-                  const float sa = colval(sa_lo, sa_hi, c + j);
-                  const float rw = colval(rw_lo, rw_hi, c + j);
-                  if (col < t.rows) {
-                    const int64_t row = (int64_t)t.row0 + col;
-                    const float o = s.i8 ? (float)(int32_t)va[j] * (sw0 * sa) : __uint_as_float(va[j]);
-                    p.O[row * p.d + n] = f2bf(o * rw);
-                    if (two) {
-                      const float o1 = s.i8 ? (float)(int32_t)vb[j] * (sw1 * sa) : __uint_as_float(vb[j]);
-                      p.O[row * p.d + n1] = f2bf(o1 * rw);
-                    }
-                  }
-                }
+            for (int j = 0; j < 8; j += 2) {
+              const float2 a2 = fmul2(make_float2((float)(int32_t)va[j], (float)(int32_t)va[j + 1]), fmul2(swa, s2[j / 2]));
+              const float2 b2 = fmul2(make_float2((float)(int32_t)vb[j], (float)(int32_t)vb[j + 1]), fmul2(swb, s2[j / 2]));
+              fa[j] = a2.x; fa[j + 1] = a2.y; fb[j] = b2.x; fb[j + 1] = b2.y;
+            }
+          }
+          if (t.phase == 0) {
+            uint16_t hb[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hb[j] = f2bf(silu_f(fa[j]) * fb[j]);
+            emit_h8(p, t, dmode, dqmax, n, col0 + c, nvalid - c, hb, ctl, wg, q, lane, rbuf);
+          } else {
+            const float4 r0 = *reinterpret_cast<const float4*>(cw_rw + c);
+            const float4 r1 = *reinterpret_cast<const float4*>(cw_rw + c + 4);
+            const float rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            uint16_t* o0 = p.O + ((int64_t)t.row0 + col0 + c) * p.d + n;
+            uint16_t* o1 = p.O + ((int64_t)t.row0 + col0 + c) * p.d + n1;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (c + j < nvalid) {
+                o0[(int64_t)j * p.d] = f2bf(fa[j] * rw[j]);
+                if (two) o1[(int64_t)j * p.d] = f2bf(fb[j] * rw[j]);
               }
             }
-          } else {
-            // ---- register-accumulating epilogue (g128 drains / hetero gate-up)
-            const bool dst_hi = t.phase == 0 && nsl == 2 && si == 1;  // hetero: the up sub-loop
-            const uint32_t aA = lane_addr + colA + (uint32_t)col0, aB = lane_addr + colB + (uint32_t)col0;
-            float* sa_w = ctl.sa[ew];
+          }
+        }
+#endif
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl.acce[b0]);
+      } else {
+        // ======== register-accumulating epilogue (g128 drains / hetero gate-up sub-loops)
+        float2 acc2[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc2[i] = make_float2(0.f, 0.f);
+        for (int si = 0; si < nsl; ++si) {
+          const SubLoop s = sl[si];
+          const bool two = s.nmats == 2;
+          const int nev = s.g128 ? s.ns : 1;
+          const float* xs_s = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;  // group-major [g][R]
+          const uint16_t* wsc0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off);
+          const uint16_t* wsc1 =
+              two ? reinterpret_cast<const uint16_t*>(s.mat[1]->packed + s.mat[1]->geo.wa_scale_off) : wsc0;
+          const int64_t wN = s.mat[0]->geo.N;
+          const float* xs_lo = xs_s + (int64_t)t.row0 + cl;
+          const float* xs_hi = xs_s + (int64_t)t.row0 + ch;
+          const int64_t gs = p.hs_stride;
+          // phase 0: scales written before this kernel, prefetched one event ahead (read-only path);
+          // phase 2: h-scales written by this kernel, read after the accumulator wait through L2 (ld.cg)
+          const bool pre = t.phase == 0;
+          float nsw0 = 1.f, nsw1 = 1.f, nsa_lo = 1.f, nsa_hi = 1.f;
+          if (s.i8 && pre) {
+            nsw0 = bf16f(__ldg(wsc0 + n));
+            if (two) nsw1 = bf16f(__ldg(wsc1 + n1));
+            nsa_lo = vlo ? __ldg(xs_lo) : 0.f;
+            nsa_hi = vhi ? __ldg(xs_hi) : 0.f;
+          }
+          for (int ev = 0; ev < nev; ++ev) {
+            float sw0 = nsw0, sw1 = nsw1, sa_lo = nsa_lo, sa_hi = nsa_hi;
+            const uint32_t b0 = abuf;
+            abuf = (abuf + 1) & (kAccBufs - 1);
+            twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
+            acc_ph ^= 1u << b0;
+            tc_fence_after();
+            if (s.i8 && !pre) {
+              sw0 = bf16f(__ldg(wsc0 + (int64_t)ev * wN + n));
+              if (two) sw1 = bf16f(__ldg(wsc1 + (int64_t)ev * wN + n1));
+              sa_lo = vlo ? __ldcg(xs_lo + ev * gs) : 0.f;
+              sa_hi = vhi ? __ldcg(xs_hi + ev * gs) : 0.f;
+            }
+            if (s.i8 && pre && ev + 1 < nev) {
+              nsw0 = bf16f(__ldg(wsc0 + (int64_t)(ev + 1) * wN + n));
+              if (two) nsw1 = bf16f(__ldg(wsc1 + (int64_t)(ev + 1) * wN + n1));
+              nsa_lo = vlo ? __ldg(xs_lo + (ev + 1) * gs) : 0.f;
+              nsa_hi = vhi ? __ldg(xs_hi + (ev + 1) * gs) : 0.f;
+            }
             if (s.i8) {
               __syncwarp();  // previous event's broadcast reads are done
-              sa_w[lane] = sa_lo;
-              sa_w[32 + lane] = sa_hi;
+              cw_sa[lane] = sa_lo;
+              cw_sa[32 + lane] = sa_hi;
               __syncwarp();
             }
+            const uint32_t colA = b0 * (uint32_t)kAccCols;
+            const uint32_t colB = colA + (uint32_t)kMat1Col;
+            const bool dst_hi = t.phase == 0 && nsl == 2 && si == 1;  // hetero: the up sub-loop
+            const uint32_t aA = lane_addr + colA + (uint32_t)col0, aB = lane_addr + colB + (uint32_t)col0;
+#ifndef MXM_ABL_EPI
             if (dst_hi)
-              drain_event_any<16>(half, acc2, aA, aB, s.i8, false, s.g128, sw0, sw1, sa_w);
+              drain_event_any<16>(half, acc2, aA, aB, s.i8, false, s.g128, sw0, sw1, cw_sa);
             else
-              drain_event_any<0>(half, acc2, aA, aB, s.i8, two, s.g128, sw0, sw1, sa_w);
+              drain_event_any<0>(half, acc2, aA, aB, s.i8, two, s.g128, sw0, sw1, cw_sa);
+#endif
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl.acce[b0]);
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl.acce[b0]);
         }
-      }
-      if (reg_mode) {
         const float* acc = reinterpret_cast<const float*>(acc2);
         if (t.phase == 0) {
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
             if (cc * 8 < half) {
-              float h[8];
+              uint16_t hb[8];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) h[j] = silu_f(acc[cc * 8 + j]) * acc[32 + cc * 8 + j];
-              emit_h8(p, t, dmode, dqmax, n, col0 + cc * 8, h, ctl, wg, q, lane, rbuf);
+              for (int j = 0; j < 8; ++j) hb[j] = f2bf(silu_f(acc[cc * 8 + j]) * acc[32 + cc * 8 + j]);
+              emit_h8(p, t, dmode, dqmax, n, col0 + cc * 8, nvalid - cc * 8, hb, ctl, wg, q, lane, rbuf);
             }
           }
         } else {
-          float rw_lo = 0.f, rw_hi = 0.f;
-          const int cl = col0 + lane, ch = col0 + 32 + lane;
-          rw_lo = (lane < half && cl < t.rows) ? __ldg(p.row_w + t.row0 + cl) : 0.f;
-          rw_hi = (32 + lane < half && ch < t.rows) ? __ldg(p.row_w + t.row0 + ch) : 0.f;
           const bool two = sl[0].nmats == 2;  // paired down tiles: mat 1 in acc[32..63]
-#pragma unroll 1
-          for (int c = 0; c < half; ++c) {
-            const int col = col0 + c;
-            const float rw = colval(rw_lo, rw_hi, c);
-            if (col < t.rows) {
-              p.O[((int64_t)t.row0 + col) * p.d + n] = f2bf(acc[c] * rw);
-              if (two) p.O[((int64_t)t.row0 + col) * p.d + n1] = f2bf(acc[32 + c] * rw);
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            if (cc * 8 < half) {
+              const float4 r0 = *reinterpret_cast<const float4*>(cw_rw + cc * 8);
+              const float4 r1 = *reinterpret_cast<const float4*>(cw_rw + cc * 8 + 4);
+              const float rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+              uint16_t* o0 = p.O + ((int64_t)t.row0 + col0 + cc * 8) * p.d + n;
+              uint16_t* o1 = p.O + ((int64_t)t.row0 + col0 + cc * 8) * p.d + n1;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (cc * 8 + j < nvalid) {
+                  o0[(int64_t)j * p.d] = f2bf(acc[cc * 8 + j] * rw[j]);
+                  if (two && cc < 4) o1[(int64_t)j * p.d] = f2bf(acc[32 + cc * 8 + j] * rw[j]);
+                }
+              }
             }
           }
         }

@@ -17,10 +17,11 @@ struct GemmParams {
   int32_t* hq_done;
   const int32_t* grp_n1;
   const int32_t* grp_nq;
-  const float* xs[3];  // activation scales of the gate/up input slots (index 1, 2)
+  const float* xs[3];  // activation scales of the gate/up input slots (index 1, 2), group-major [g][R]
   uint16_t* H;
   int8_t* Hq;
-  float* Hs;
+  float* Hs;           // h scales, group-major [g][R]
+  int64_t hs_stride;   // R: rows of the workspace (stride between activation-scale groups)
   uint32_t* hmax;  // per route row: max |h| (fp32 bits) for per-token W-A downs (order-independent atomicMax)
   uint16_t* O;
   const float* row_w;

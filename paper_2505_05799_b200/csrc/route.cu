@@ -151,12 +151,12 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
       for (int i = lane; i < d / 8; i += 32) d4[i] = s4[i];
     } else {
       int8_t* q = (L.in_slot == 1 ? XqA : XqB) + row * d;
-      float* sc = (L.in_slot == 1 ? XsA : XsB) + row * (d / 128);
+      float* sc = (L.in_slot == 1 ? XsA : XsB) + row;  // group-major [g][R]
       const int g = L.a_group == -1 ? d : L.a_group;
       const int qmax = (1 << (L.a_bits - 1)) - 1;
       for (int gi = 0; gi < d / g; ++gi) {
         const float s = quant_group_warp(src + gi * g, q + gi * g, g, qmax, nullptr);
-        if (lane == 0) sc[gi] = s;
+        if (lane == 0) sc[gi * R] = s;
       }
     }
   }

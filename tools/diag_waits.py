@@ -1,5 +1,9 @@
 """Per-wait-site cycle breakdown of the persistent kernel (dev tool): python tools/diag_waits.py CFG TABLE [T]."""
 import os, sys
+# the counters exist only in a -DMXM_DEBUG_COUNTERS build: tools/variants/lib_diag.so (built on demand)
+_here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if "MXM_LIB" not in os.environ:
+    os.environ["MXM_LIB"] = os.path.join(_here, "tools", "variants", "lib_diag.so")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from synth import configs as C
