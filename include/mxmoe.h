@@ -85,6 +85,8 @@ mxm_status mxm_act_quant(const void* v_bf16, int64_t M, int64_t K, int32_t a_bit
  *   perm    int32[T*k]    perm[p] = t*k + j of the route at sorted position p (stable in (t, j) order);
  *                         entries >= offsets[E] are left untouched
  *   err     int32 device word, set to MXM_E_DATA for an id outside [-1, E) (that route is skipped) */
+/* [sync] device scratch bytes mxm_route_prep needs for T tokens, top-k k, E experts. */
+mxm_status mxm_route_scratch_bytes(int64_t T, int32_t k, int32_t E, int64_t* bytes);
 mxm_status mxm_route_prep(const int32_t* topk_ids, int64_t T, int32_t k, int32_t E, int32_t* counts,
                           int32_t* offsets, int32_t* perm, int32_t* err, void* scratch, int64_t scratch_bytes,
                           mxm_stream stream);
@@ -92,7 +94,9 @@ mxm_status mxm_route_prep(const int32_t* topk_ids, int64_t T, int32_t k, int32_t
 /* ---------------------------------------------------------------- layer (the per-block precision table)
  * blocks: host array [(n_routed + n_shared) * 3], order (expert-major) gate, up, down; gate/up are [inter, hidden]
  * (routed) or [shared_inter, hidden] (shared); down is [hidden, inter]. `packed` are device buffers from mxm_pack,
- * which must stay alive while the layer is used. Shared experts see every token (weight shared_w or 1). */
+ * which must stay alive while the layer is used. Shared experts see every token (weight shared_w or 1).
+ * Limits (MXM_E_CONFIG otherwise): 1 <= n_routed <= 256, 0 <= n_shared <= 32, n_routed + n_shared <= 256,
+ * hidden, inter, shared_inter multiples of 128. */
 typedef struct {
   mxm_scheme scheme;
   const void* packed;

@@ -116,8 +116,9 @@ def route_prep(topk_ids: torch.Tensor, E: int):
     offsets = torch.zeros(E + 1, dtype=torch.int32, device=dev)
     perm = torch.full((T * k,), -1, dtype=torch.int32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
-    nch = (T * k + 2047) // 2048
-    scratch = torch.empty(max(256, nch * E * 4 + 256), dtype=torch.uint8, device=dev)
+    nb = C.c_int64(0)
+    check(load().mxm_route_scratch_bytes(T, k, E, C.byref(nb)))
+    scratch = torch.empty(max(256, nb.value), dtype=torch.uint8, device=dev)
     check(load().mxm_route_prep(_ptr(topk_ids.contiguous()), T, k, E, _ptr(counts), _ptr(offsets), _ptr(perm),
                                 _ptr(err), _ptr(scratch), scratch.numel(), _stream()))
     return counts, offsets, perm, err

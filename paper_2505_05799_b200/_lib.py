@@ -47,6 +47,7 @@ SIGNATURES = {
     "mxm_pack": (C.c_int, [_S, _P, _P, _P, _I64, _I64, _P, _P]),
     "mxm_dequantize": (C.c_int, [_S, _P, _I64, _I64, _P, _P]),
     "mxm_act_quant": (C.c_int, [_P, _I64, _I64, _I32, _I32, _P, _P, _P, _P]),
+    "mxm_route_scratch_bytes": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
     "mxm_route_prep": (C.c_int, [_P, _I64, _I32, _I32, _P, _P, _P, _P, _P, _I64, _P]),
     "mxm_layer_desc_bytes": (C.c_int, [C.POINTER(mxm_layer_desc), C.POINTER(_I64)]),
     "mxm_layer_init": (C.c_int, [C.POINTER(mxm_layer_desc), _P, _I64, _P, C.POINTER(_P)]),

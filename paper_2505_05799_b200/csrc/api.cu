@@ -215,6 +215,12 @@ mxm_status mxm_act_quant(const void* v, int64_t M, int64_t K, int32_t a_bits, in
   return MXM_OK;
 }
 
+mxm_status mxm_route_scratch_bytes(int64_t T, int32_t k, int32_t E, int64_t* bytes) {
+  if (!bytes || E <= 0 || E > 256 || k <= 0 || k > 32 || T < 0) return fail(MXM_E_CONFIG, "bad E/k/T");
+  *bytes = route_scratch_bytes(T * k, E);
+  return MXM_OK;
+}
+
 mxm_status mxm_route_prep(const int32_t* topk_ids, int64_t T, int32_t k, int32_t E, int32_t* counts, int32_t* offsets,
                           int32_t* perm, int32_t* err, void* scratch, int64_t scratch_bytes, mxm_stream stream) {
   if (!topk_ids || !counts || !offsets || !perm) return fail(MXM_E_CONFIG, "null argument");
@@ -236,7 +242,7 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
   (void)tile_costs;
   if (!d || !d->blocks || !desc_dev || !out) return fail(MXM_E_CONFIG, "null argument");
   const int E = d->n_routed, S = d->n_shared, V = E + S;
-  if (E <= 0 || E > 256 || S < 0 || V > 256) return fail(MXM_E_CONFIG, "expert count out of range");
+  if (E <= 0 || E > 256 || S < 0 || S > 32 || V > 256) return fail(MXM_E_CONFIG, "expert count out of range");
   if (d->hidden <= 0 || d->hidden % 128 || d->inter <= 0 || d->inter % 128) return fail(MXM_E_CONFIG, "hidden/inter % 128");
   if (S > 0 && (d->shared_inter <= 0 || d->shared_inter % 128)) return fail(MXM_E_CONFIG, "shared_inter % 128");
   if (desc_bytes < (int64_t)sizeof(ExpertDesc) * V) return fail(MXM_E_CONFIG, "descriptor buffer too small");

@@ -45,11 +45,19 @@ constexpr int kSlotBytes = 3 * kTileBytes;  // per stage: token tile B | mat 0 (
 
 constexpr int kOffCtl = kStages * kSlotBytes;
 constexpr int kCtlBytes = 8192;
-constexpr int kSmemBytes = kOffCtl + kCtlBytes + 1024;
+// scale ring for weight-activation g128 stages (one 128-K group each): the producer bulk-copies the group's
+// weight scales (128 bf16 per mat) and activation scales (the m-tile's rows of the group-major [g][R]
+// array, from the 16-byte-aligned floor) next to the stage's operands; the epilogue drains the event's
+// accumulator against them, then releases the slot.
+constexpr int kSSlots = 4;
+constexpr int kSSlotBytes = 1024;  // [0,256) mat-0 s_w | [256,512) mat-1 s_w | [512,1024) s_a (<= 125 floats)
+constexpr int kOffScale = kOffCtl + kCtlBytes;
+constexpr int kSmemBytes = kOffScale + kSSlots * kSSlotBytes + 1024;
 
 struct Ctl {
   uint64_t full[kStages], empty[kStages];
   uint64_t aready[kASlots], aempty[kASlots];
+  uint64_t sfull[kSSlots], sempty[kSSlots];
   uint64_t accf[kAccBufs], acce[kAccBufs];
   uint64_t tfull[kRing], tempty[kRing];
   Task ring[kRing];
@@ -106,6 +114,13 @@ __device__ __forceinline__ int build_subloops(const Task& t, const ExpertDesc* _
 }
 
 __device__ __forceinline__ int nt_index(int nt) { return nt <= 16 ? 0 : (nt <= 32 ? 1 : (nt <= 64 ? 2 : 3)); }
+
+// activation scales of group g for rows [row0, row0 + nt): 16-byte-aligned source span and element offset
+__device__ __forceinline__ const float* ascale_span(const float* base, int64_t R, int g, int row0, uint32_t& off) {
+  const float* p = base + (int64_t)g * R + row0;
+  off = (uint32_t)(((uintptr_t)p & 15u) >> 2);
+  return p - off;
+}
 
 // ---------------------------------------------------------------- transforms (one thread per A row)
 __device__ __forceinline__ uint32_t bf2_sub(uint32_t a, uint32_t b) {
@@ -305,24 +320,24 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 template <int HALF, int DST0>
 __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8, bool two,
                                             bool small, float sw0, float sw1, const float* sa) {
-  constexpr int CH = 8;
+  constexpr int CH = 8;  // 16-wide staging + 64 accumulators exceeds the 128-register epilogue budget (spills)
   constexpr float kMagic = 12582912.f;  // 2^23 + 2^22
 #pragma unroll
   for (int c0 = 0; c0 < HALF; c0 += CH) {
-    uint32_t va[8], vb[8];
+    uint32_t va[CH], vb[CH];
     tmem_ld8(addrA + c0, va);
     if (two) tmem_ld8(addrB + c0, vb);
     tmem_ld_wait();
     if (i8) {
-      const float4 s4a = *reinterpret_cast<const float4*>(sa + c0);
-      const float4 s4b = *reinterpret_cast<const float4*>(sa + c0 + 4);
-      const float2 sac[4] = {make_float2(s4a.x, s4a.y), make_float2(s4a.z, s4a.w), make_float2(s4b.x, s4b.y),
-                             make_float2(s4b.z, s4b.w)};
 #pragma unroll
       for (int j = 0; j < CH; j += 2) {
         const int col = c0 + j;
+        const float2 sac = make_float2(sa[col], sa[col + 1]);
         float2 fa, fb;
-        if (small) {
+#ifndef MXM_MAGIC_I2F
+#define MXM_MAGIC_I2F 0  // sm_100 converts with I2FP.F32.S32; the 2^23+2^22 add is an A/B alternative
+#endif
+        if (MXM_MAGIC_I2F && small) {
           fa = fadd2(make_float2(__int_as_float((int32_t)va[j] + 0x4B400000), __int_as_float((int32_t)va[j + 1] + 0x4B400000)),
                      make_float2(-kMagic, -kMagic));
           fb = fadd2(make_float2(__int_as_float((int32_t)vb[j] + 0x4B400000), __int_as_float((int32_t)vb[j + 1] + 0x4B400000)),
@@ -331,8 +346,8 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
           fa = make_float2((float)(int32_t)va[j], (float)(int32_t)va[j + 1]);
           fb = make_float2((float)(int32_t)vb[j], (float)(int32_t)vb[j + 1]);
         }
-        acc2[DST0 + col / 2] = ffma2(fa, fmul2(make_float2(sw0, sw0), sac[j / 2]), acc2[DST0 + col / 2]);
-        if (two) acc2[16 + col / 2] = ffma2(fb, fmul2(make_float2(sw1, sw1), sac[j / 2]), acc2[16 + col / 2]);
+        acc2[DST0 + col / 2] = ffma2(fa, fmul2(make_float2(sw0, sw0), sac), acc2[DST0 + col / 2]);
+        if (two) acc2[16 + col / 2] = ffma2(fb, fmul2(make_float2(sw1, sw1), sac), acc2[16 + col / 2]);
       }
     } else {
 #pragma unroll
@@ -557,6 +572,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       mbar_init(&ctl.aready[i], kXfWarps);
       mbar_init(&ctl.aempty[i], 1);
     }
+    for (int i = 0; i < kSSlots; ++i) {
+      mbar_init(&ctl.sfull[i], 1);
+      mbar_init(&ctl.sempty[i], 8);  // the 8 epilogue warps
+    }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&ctl.accf[i], 1);
       mbar_init(&ctl.acce[i], 8);
@@ -605,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   if (warp == 0) {
     // =========================== producer
     if (lane == 0) {
-      uint32_t stage = 0, sphase = 0;
+      uint32_t stage = 0, sphase = 0, sidx = 0;
       for (uint32_t it = 0;; ++it) {
         const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
         const int idx = atomicAdd(&p.meta[5], 1);
@@ -664,6 +683,25 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               src1 += c1;
             }
             tma_load_2d(tileB(stage), map, &ctl.full[stage], ks * kstep, t.row0);
+            if (s.g128) {  // the 128-K group's scales into the scale ring (read by the epilogue)
+              const uint32_t ss = sidx & (kSSlots - 1);
+              twait(&ctl.sempty[ss], ((sidx / kSSlots) & 1) ^ 1, pc[1], prof_on);
+              uint8_t* dst = smem + kOffScale + ss * kSSlotBytes;
+              const float* abase = t.phase == 0 ? p.xs[s.mat[0]->in_slot] : p.Hs;
+              uint32_t aoff;
+              const float* asrc = ascale_span(abase, p.hs_stride, ks, t.row0, aoff);
+              const uint32_t abytes = ((aoff + t.nt) * 4u + 15u) & ~15u;
+              const uint32_t wbytes = 256u * (uint32_t)s.nmats;
+              mbar_arrive_expect_tx(&ctl.sfull[ss], wbytes + abytes);
+              const uint8_t* w0 = s.mat[0]->packed + g0.wa_scale_off + ((int64_t)ks * g0.N + s.tile[0] * 128) * 2;
+              bulk_load(dst, w0, 256u, &ctl.sfull[ss]);
+              if (s.nmats == 2) {
+                const uint8_t* w1 = s.mat[1]->packed + g1.wa_scale_off + ((int64_t)ks * g1.N + s.tile[1] * 128) * 2;
+                bulk_load(dst + 256, w1, 256u, &ctl.sfull[ss]);
+              }
+              bulk_load(dst + 512, asrc, abytes, &ctl.sfull[ss]);
+              ++sidx;
+            }
             if (++stage == kStages) {
               stage = 0;
               sphase ^= 1;
@@ -801,7 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 #endif
     const int ew = warp - 8, wg = ew >> 2, q = warp & 3;
     const int l = q * 32 + lane;  // output channel within the tile == TMEM lane
-    uint32_t abuf = 0, acc_ph = 0, rbuf = 0;
+    uint32_t abuf = 0, acc_ph = 0, rbuf = 0, sidx = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
       twait(&ctl.tfull[slot], rphase, pc[9], prof_on);
@@ -977,43 +1015,50 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const uint16_t* wsc0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off);
           const uint16_t* wsc1 =
               two ? reinterpret_cast<const uint16_t*>(s.mat[1]->packed + s.mat[1]->geo.wa_scale_off) : wsc0;
-          const int64_t wN = s.mat[0]->geo.N;
           const float* xs_lo = xs_s + (int64_t)t.row0 + cl;
           const float* xs_hi = xs_s + (int64_t)t.row0 + ch;
           const int64_t gs = p.hs_stride;
-          // phase 0: scales written before this kernel, prefetched one event ahead (read-only path);
-          // phase 2: h-scales written by this kernel, read after the accumulator wait through L2 (ld.cg)
+          // g128: per-event scales come through the scale ring. Per-channel: phase 0 reads scales written
+          // before this kernel (read-only path, before the wait); phase 2 reads h-scales written by this
+          // kernel after the accumulator wait, through L2 (ld.cg)
           const bool pre = t.phase == 0;
           float nsw0 = 1.f, nsw1 = 1.f, nsa_lo = 1.f, nsa_hi = 1.f;
-          if (s.i8 && pre) {
-            nsw0 = bf16f(__ldg(wsc0 + n));
-            if (two) nsw1 = bf16f(__ldg(wsc1 + n1));
-            nsa_lo = vlo ? __ldg(xs_lo) : 0.f;
-            nsa_hi = vhi ? __ldg(xs_hi) : 0.f;
+          if (s.i8 && !s.g128) {  // per-channel (one event): scales from global memory
+            if (pre) {
+              nsw0 = bf16f(__ldg(wsc0 + n));
+              if (two) nsw1 = bf16f(__ldg(wsc1 + n1));
+              nsa_lo = vlo ? __ldg(xs_lo) : 0.f;
+              nsa_hi = vhi ? __ldg(xs_hi) : 0.f;
+            }
           }
           for (int ev = 0; ev < nev; ++ev) {
-            float sw0 = nsw0, sw1 = nsw1, sa_lo = nsa_lo, sa_hi = nsa_hi;
+            float sw0 = nsw0, sw1 = nsw1;
             const uint32_t b0 = abuf;
             abuf = (abuf + 1) & (kAccBufs - 1);
             twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
             acc_ph ^= 1u << b0;
             tc_fence_after();
-            if (s.i8 && !pre) {
-              sw0 = bf16f(__ldg(wsc0 + (int64_t)ev * wN + n));
-              if (two) sw1 = bf16f(__ldg(wsc1 + (int64_t)ev * wN + n1));
-              sa_lo = vlo ? __ldcg(xs_lo + ev * gs) : 0.f;
-              sa_hi = vhi ? __ldcg(xs_hi + ev * gs) : 0.f;
-            }
-            if (s.i8 && pre && ev + 1 < nev) {
-              nsw0 = bf16f(__ldg(wsc0 + (int64_t)(ev + 1) * wN + n));
-              if (two) nsw1 = bf16f(__ldg(wsc1 + (int64_t)(ev + 1) * wN + n1));
-              nsa_lo = vlo ? __ldg(xs_lo + (ev + 1) * gs) : 0.f;
-              nsa_hi = vhi ? __ldg(xs_hi + (ev + 1) * gs) : 0.f;
-            }
-            if (s.i8) {
-              __syncwarp();  // previous event's broadcast reads are done
-              cw_sa[lane] = sa_lo;
-              cw_sa[32 + lane] = sa_hi;
+            const float* sa_ev = cw_sa;
+            uint32_t ss = 0;
+            if (s.g128) {  // g128 event: the group's scales arrived in the scale ring with the stage
+              ss = sidx & (kSSlots - 1);
+              twait(&ctl.sfull[ss], (sidx / kSSlots) & 1, pc[10], prof_on);
+              const uint8_t* slotp = smem + kOffScale + ss * kSSlotBytes;
+              sw0 = bf16f(reinterpret_cast<const uint16_t*>(slotp)[l]);
+              if (two) sw1 = bf16f(reinterpret_cast<const uint16_t*>(slotp + 256)[l]);
+              uint32_t aoff;
+              (void)ascale_span(xs_s, gs, ev, t.row0, aoff);
+              sa_ev = reinterpret_cast<const float*>(slotp + 512) + aoff + col0;
+            } else if (s.i8) {
+              if (!pre) {  // h-scales are written by this kernel: read after the MMA consumed Hq (ld.cg)
+                sw0 = bf16f(__ldg(wsc0 + n));
+                if (two) sw1 = bf16f(__ldg(wsc1 + n1));
+                nsa_lo = vlo ? __ldcg(xs_lo) : 0.f;
+                nsa_hi = vhi ? __ldcg(xs_hi) : 0.f;
+              }
+              __syncwarp();
+              cw_sa[lane] = nsa_lo;
+              cw_sa[32 + lane] = nsa_hi;
               __syncwarp();
             }
             const uint32_t colA = b0 * (uint32_t)kAccCols;
@@ -1022,13 +1067,17 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             const uint32_t aA = lane_addr + colA + (uint32_t)col0, aB = lane_addr + colB + (uint32_t)col0;
 #ifndef MXM_ABL_EPI
             if (dst_hi)
-              drain_event_any<16>(half, acc2, aA, aB, s.i8, false, s.g128, sw0, sw1, cw_sa);
+              drain_event_any<16>(half, acc2, aA, aB, s.i8, false, s.g128, sw0, sw1, sa_ev);
             else
-              drain_event_any<0>(half, acc2, aA, aB, s.i8, two, s.g128, sw0, sw1, cw_sa);
+              drain_event_any<0>(half, acc2, aA, aB, s.i8, two, s.g128, sw0, sw1, sa_ev);
 #endif
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&ctl.acce[b0]);
+            if (lane == 0) {
+              mbar_arrive(&ctl.acce[b0]);
+              if (s.g128) mbar_arrive(&ctl.sempty[ss]);
+            }
+            if (s.g128) ++sidx;
           }
         }
         const float* acc = reinterpret_cast<const float*>(acc2);

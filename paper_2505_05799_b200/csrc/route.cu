@@ -16,7 +16,7 @@
 
 namespace mxm {
 
-constexpr int kRouteChunk = 2048;
+constexpr int kRouteChunk = 256;  // one placement round per block: 96 blocks at T*k = 24576
 constexpr int kMaxExperts = 1024;
 
 // ---- S1a: per-chunk histograms; invalid ids -> error word
@@ -39,48 +39,79 @@ __global__ void route_count_kernel(const int32_t* __restrict__ ids, int64_t n, i
   for (int e = threadIdx.x; e < E; e += blockDim.x) chunk_hist[(int64_t)blockIdx.x * E + e] = hist[e];
 }
 
-// ---- S1b: single block: chunk bases, counts, offsets, virtual-expert row offsets
-__global__ void route_scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E, int S, int64_t T,
-                                  int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
-                                  int32_t* __restrict__ v_off) {
-  __shared__ int32_t tot[kMaxExperts];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int32_t run = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const int32_t h = chunk_hist[(int64_t)c * E + e];
-      chunk_hist[(int64_t)c * E + e] = run;  // becomes the chunk's base within expert e
-      run += h;
-    }
-    tot[e] = run;
-    if (counts) counts[e] = run;
+// ---- S1b: one warp per expert: exclusive scan of its per-chunk counts (lane = contiguous chunk range)
+__global__ void route_scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E, int32_t* __restrict__ counts) {
+  const int e = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (e >= E) return;
+  const int per = (nchunks + 31) / 32;
+  const int c0 = min(nchunks, lane * per), c1 = min(nchunks, c0 + per);
+  int32_t sum = 0;
+  for (int c = c0; c < c1; ++c) sum += chunk_hist[(int64_t)c * E + e];
+  int32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
+  int32_t run = incl - sum;
+  for (int c = c0; c < c1; ++c) {
+    const int32_t h = chunk_hist[(int64_t)c * E + e];
+    chunk_hist[(int64_t)c * E + e] = run;  // becomes the chunk's base within expert e
+    run += h;
+  }
+  if (lane == 31 && counts) counts[e] = incl;
+}
+
+// exclusive scan of counts[0..E) (E <= 256) into smem `off` by a 256-thread block; returns the total
+__device__ int32_t block_scan_counts(const int32_t* __restrict__ counts, int E, int32_t* off, int32_t* wtot) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int32_t v = t < E ? counts[t] : 0;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wtot[w] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t run = 0;
-    for (int e = 0; e < E; ++e) {
-      if (offsets) offsets[e] = run;
-      if (v_off) v_off[e] = (int32_t)(S * T) + run;
-      run += tot[e];
-    }
-    if (offsets) offsets[E] = run;
-    if (v_off) {
-      v_off[E + S] = (int32_t)(S * T) + run;  // end of routed rows
-      for (int s = 0; s < S; ++s) v_off[E + s] = (int32_t)(s * T);
-    }
+  int32_t before = 0, total = 0;
+  for (int i = 0; i < 8; ++i) {
+    if (i < w) before += wtot[i];
+    total += wtot[i];
   }
+  if (t < E) off[t] = before + x - v;
+  __syncthreads();
+  return total;
 }
 
 // ---- S1c: stable placement within chunk (warp match + per-warp counts)
 __global__ void route_place_kernel(const int32_t* __restrict__ ids, const float* __restrict__ topk_w, int64_t n, int k,
-                                   int E, int64_t row_base, const int32_t* __restrict__ chunk_base,
-                                   const int32_t* __restrict__ offsets_or_null, const int32_t* __restrict__ v_off,
-                                   int32_t* __restrict__ perm, int32_t* __restrict__ row_src,
-                                   float* __restrict__ row_w, int32_t* __restrict__ row_exp, int32_t* __restrict__ inv) {
+                                   int E, int S, int64_t T, const int32_t* __restrict__ chunk_base,
+                                   const int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
+                                   int32_t* __restrict__ v_off, int32_t* __restrict__ perm,
+                                   int32_t* __restrict__ row_src, float* __restrict__ row_w,
+                                   int32_t* __restrict__ row_exp, int32_t* __restrict__ inv) {
   __shared__ int32_t base[kMaxExperts];
   __shared__ int32_t wcnt[8][kMaxExperts / 4];  // 8 warps; E <= 256 in this path
+  __shared__ int32_t wtot[8];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < E; e += blockDim.x)
-    base[e] = chunk_base[(int64_t)blockIdx.x * E + e] + (offsets_or_null ? offsets_or_null[e] : v_off[e] - (int32_t)row_base);
+  // expert offsets (every block recomputes the E-scan; block 0 publishes offsets / v_off)
+  const int32_t total = block_scan_counts(counts, E, base, wtot);
+  const int64_t row_base = row_src ? (int64_t)S * T : 0;  // routed rows follow the S*T shared-expert rows
+  if (blockIdx.x == 0) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      if (offsets) offsets[e] = base[e];
+      if (v_off) v_off[e] = (int32_t)row_base + base[e];
+    }
+    if (threadIdx.x == 0) {
+      if (offsets) offsets[E] = total;
+      if (v_off) {
+        v_off[E + S] = (int32_t)row_base + total;  // end of routed rows
+        for (int s = 0; s < S; ++s) v_off[E + s] = (int32_t)(s * T);
+      }
+    }
+  }
+  for (int e = threadIdx.x; e < E; e += blockDim.x) base[e] += chunk_base[(int64_t)blockIdx.x * E + e];
   const int64_t c0 = (int64_t)blockIdx.x * kRouteChunk;
   for (int sub = 0; sub < kRouteChunk; sub += 256) {
     for (int i = threadIdx.x; i < 8 * E; i += blockDim.x) wcnt[i / E][i % E] = 0;
@@ -162,31 +193,39 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
   }
 }
 
-// ---- S8: combine, one block per token
+// ---- S8: combine, one block per token; all k + S source rows are resolved first so their loads overlap
 __global__ void combine_kernel(const uint16_t* __restrict__ O, int d, int64_t T, int k, int S,
                                const int32_t* __restrict__ inv, uint16_t* __restrict__ y) {
   const int64_t t = blockIdx.x;
+  __shared__ int32_t rows[64];
+  if (threadIdx.x < k + S) {
+    const int j = threadIdx.x;
+    rows[j] = j < k ? inv[t * k + j] : (int32_t)((j - k) * T + t);  // routed rows, then shared rows
+  }
+  __syncthreads();
+  const int n = k + S;
+  auto add = [](float (&acc)[8], uint4 u) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[2 * i] += bf16_bits_to_float(w[i] & 0xFFFFu);
+      acc[2 * i + 1] += bf16_bits_to_float(w[i] >> 16);
+    }
+  };
   for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < k; ++j) {
-      const int32_t row = inv[t * k + j];
-      if (row < 0) continue;
-      uint4 v = reinterpret_cast<const uint4*>(O + (int64_t)row * d)[c];
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    constexpr int kBatch = 8;  // loads in flight per thread before the (fixed-order) sum
+    for (int j0 = 0; j0 < n; j0 += kBatch) {
+      uint4 v[kBatch];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        acc[2 * i] += bf16_bits_to_float(w[i] & 0xFFFFu);
-        acc[2 * i + 1] += bf16_bits_to_float(w[i] >> 16);
+      for (int j = 0; j < kBatch; ++j) {
+        v[j] = make_uint4(0, 0, 0, 0);
+        if (j0 + j < n && rows[j0 + j] >= 0)
+          v[j] = __ldcs(reinterpret_cast<const uint4*>(O + (int64_t)rows[j0 + j] * d) + c);
       }
-    }
-    for (int s = 0; s < S; ++s) {
-      uint4 v = reinterpret_cast<const uint4*>(O + (s * T + t) * d)[c];
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        acc[2 * i] += bf16_bits_to_float(w[i] & 0xFFFFu);
-        acc[2 * i + 1] += bf16_bits_to_float(w[i] >> 16);
-      }
+      for (int j = 0; j < kBatch; ++j)
+        if (j0 + j < n && rows[j0 + j] >= 0) add(acc, v[j]);
     }
     uint32_t out[4];
 #pragma unroll
@@ -215,11 +254,9 @@ cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T
   if (nch > 0) {
     route_count_kernel<<<nch, 256, 0, st>>>(ids, n, E, hist, err);
   }
-  route_scan_kernel<<<1, 256, 0, st>>>(hist, nch, E, S, T, counts, offsets, v_off);
-  if (nch > 0) {
-    route_place_kernel<<<nch, 256, 0, st>>>(ids, topk_w, n, k, E, row_src ? (int64_t)S * T : 0, hist,
-                                            row_src ? nullptr : offsets, v_off, perm, row_src, row_w, row_exp, inv);
-  }
+  route_scan_kernel<<<(E + 7) / 8, 256, 0, st>>>(hist, nch, E, counts);
+  route_place_kernel<<<nch > 0 ? nch : 1, 256, 0, st>>>(ids, topk_w, n, k, E, S, T, hist, counts, offsets, v_off,
+                                                        perm, row_src, row_w, row_exp, inv);
   if (row_src && S > 0 && T > 0) {
     route_shared_kernel<<<(unsigned)((T * S + 255) / 256), 256, 0, st>>>(T, E, S, shared_w, row_src, row_w, row_exp);
   }
