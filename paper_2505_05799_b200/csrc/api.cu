@@ -494,3 +494,8 @@ mxm_status mxm_debug_task_stats(const mxm_layer* l, const void* ws, int64_t T, i
 }
 
 }  // extern "C"
+
+#ifdef MXM_DEBUG_NAN
+namespace mxm { cudaError_t debug_nan_info(unsigned long long* out, bool reset); }
+extern "C" int mxm_debug_nan_info(unsigned long long* out) { return (int)mxm::debug_nan_info(out, true); }
+#endif

@@ -122,6 +122,20 @@ __device__ __forceinline__ const float* ascale_span(const float* base, int64_t R
   return p - off;
 }
 
+#ifdef MXM_DEBUG_NAN
+// first non-finite value seen: [site, expert, phase, ntile, ks, row0, block, extra] at prof[148*16 ..]
+__device__ unsigned long long g_nan_info[8];
+__device__ __forceinline__ void nan_note(unsigned long long*, int site, const Task& t, int ks, int extra) {
+  unsigned long long* info = g_nan_info;
+  if (atomicCAS(info, 0ull, (unsigned long long)site) == 0ull) {
+    info[1] = t.expert; info[2] = t.phase; info[3] = t.ntile; info[4] = ks; info[5] = t.row0; info[6] = blockIdx.x;
+    info[7] = (unsigned long long)(unsigned)extra;
+  }
+}
+__device__ __forceinline__ bool bf2_nonfinite(uint32_t v) {
+  return ((v >> 7) & 0xFFu) == 0xFFu || ((v >> 23) & 0xFFu) == 0xFFu;
+}
+#endif
 // ---------------------------------------------------------------- transforms (one thread per A row)
 __device__ __forceinline__ uint32_t bf2_sub(uint32_t a, uint32_t b) {
   __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a), y = *reinterpret_cast<__nv_bfloat162*>(&b);
@@ -249,31 +263,24 @@ __device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, int r,
   }
 }
 
-// one transform warpgroup's share (K half H) of one stage: both mats -> TMEM A ring
+// one transform warpgroup's share (K half H) of one stage: both mats -> registers (oa, ob), stored to the TMEM A
+// ring by the caller once the MMA has released the slot (the unpack overlaps the MMAs still reading it)
 template <int H>
-__device__ __forceinline__ void xform_stage(const SubLoop& s, const uint8_t* x0, const uint8_t* x1, uint32_t tA, int r,
-                                            bool hmA, bool hmB, int bitsA, int bitsB, int mbA, int mbB, bool symA,
-                                            bool symB, uint32_t offA, uint32_t offB, bool xa, bool xb, uint32_t& sa,
-                                            uint32_t& za, uint32_t& sb, uint32_t& zb) {
-  uint32_t o[16];
+__device__ __forceinline__ void xform_stage(const SubLoop& s, const uint8_t* x0, const uint8_t* x1, int r, bool hmA,
+                                            bool hmB, int bitsA, int bitsB, int mbA, int mbB, bool symA, bool symB,
+                                            uint32_t offA, uint32_t offB, bool xa, bool xb, uint32_t& sa,
+                                            uint32_t& za, uint32_t& sb, uint32_t& zb, uint32_t (&oa)[16],
+                                            uint32_t (&ob)[16]) {
   if (s.i8) {
     if (xa) {
-      if (bitsA == 4) xform_wa<4, H>(x0, r, o); else xform_wa<5, H>(x0, r, o);
-      tmem_st16(tA + 16 * H, o);
+      if (bitsA == 4) xform_wa<4, H>(x0, r, oa); else xform_wa<5, H>(x0, r, oa);
     }
     if (xb) {
-      if (bitsB == 4) xform_wa<4, H>(x1, r, o); else xform_wa<5, H>(x1, r, o);
-      tmem_st16(tA + 32 + 16 * H, o);
+      if (bitsB == 4) xform_wa<4, H>(x1, r, ob); else xform_wa<5, H>(x1, r, ob);
     }
   } else {
-    if (xa) {
-      xform_wo_any<H>(bitsA, x0, hmA, mbA, symA, offA, r, sa, za, o);
-      tmem_st16(tA + 16 * H, o);
-    }
-    if (xb) {
-      xform_wo_any<H>(bitsB, x1, hmB, mbB, symB, offB, r, sb, zb, o);
-      tmem_st16(tA + 32 + 16 * H, o);
-    }
+    if (xa) xform_wo_any<H>(bitsA, x0, hmA, mbA, symA, offA, r, sa, za, oa);
+    if (xb) xform_wo_any<H>(bitsB, x1, hmB, mbB, symB, offB, r, sb, zb, ob);
   }
 }
 
@@ -566,7 +573,13 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&ctl.full[i], 1);
-      mbar_init(&ctl.empty[i], 1);
+      // a stage is refilled only after the MMA consumed it AND every transform warp passed it: the transform
+      // skips weight-image (SS) stages, and without its arrival it could run more than a ring cycle ahead of the
+      // producer and pass a full-barrier parity wait one phase early (stale operands)
+#ifndef MXM_EMPTY_XF
+#define MXM_EMPTY_XF 1  // 0 only for timing A/B on layers without weight-image stages (unsafe otherwise)
+#endif
+      mbar_init(&ctl.empty[i], MXM_EMPTY_XF ? 1 + kXfWarps : 1);
     }
     for (int i = 0; i < kASlots; ++i) {
       mbar_init(&ctl.aready[i], kXfWarps);
@@ -796,29 +809,44 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const bool hmA = gca == 0, hmB = gcb == 0;
           if (++gca == gstA) gca = 0;
           if (++gcb == gstB) gcb = 0;
-          if (s.xform) {
+          twait(&ctl.full[stage], sphase, pc[8], prof_on);
+          if (!s.xform) {
+            __syncwarp();
+            if (MXM_EMPTY_XF && lane == 0) mbar_arrive(&ctl.empty[stage]);
+          } else {
             const uint32_t aslot = aidx & (kASlots - 1);
-            twait(&ctl.aempty[aslot], ((aidx / kASlots) & 1) ^ 1, pc[8], prof_on);  // MMA done with the slot
-            twait(&ctl.full[stage], sphase, pc[8], prof_on);
-            tc_fence_after();
+#ifndef MXM_XF_EARLY
+#define MXM_XF_EARLY 1  // 1: unpack before waiting for the A slot (overlaps the MMAs still reading it)
+#endif
+#if !MXM_XF_EARLY
+            twait(&ctl.aempty[aslot], ((aidx / kASlots) & 1) ^ 1, pc[8], prof_on);
+#endif
             // dequantized / unpacked rows go to the TMEM A ring (lane = row); one tcgen05.st per mat and K half
             const uint32_t tA = tmem + ((uint32_t)(r & ~31) << 16) + kTmemA + aslot * 64u;
+            uint32_t oa[16], ob[16];
 #ifdef MXM_ABL_XFORM
-            {
-              uint32_t oz[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) oz[i] = 0x3f803f80u;
-              tmem_st16(tA + 16 * xh, oz);
-              if (s.nmats == 2) tmem_st16(tA + 32 + 16 * xh, oz);
-            }
+            for (int i = 0; i < 16; ++i) oa[i] = ob[i] = 0x3f803f80u;
             if (0)
 #endif
             if (xh)
-              xform_stage<1>(s, tileX(stage, 0), tileX(stage, 1), tA, r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
-                             offA, offB, xa, xb, sa, za, sb, zb);
+              xform_stage<1>(s, tileX(stage, 0), tileX(stage, 1), r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
+                             offA, offB, xa, xb, sa, za, sb, zb, oa, ob);
             else
-              xform_stage<0>(s, tileX(stage, 0), tileX(stage, 1), tA, r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
-                             offA, offB, xa, xb, sa, za, sb, zb);
+              xform_stage<0>(s, tileX(stage, 0), tileX(stage, 1), r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
+                             offA, offB, xa, xb, sa, za, sb, zb, oa, ob);
+            __syncwarp();
+            if (MXM_EMPTY_XF && lane == 0) mbar_arrive(&ctl.empty[stage]);  // this warp's smem reads are done
+#if MXM_XF_EARLY
+            twait(&ctl.aempty[aslot], ((aidx / kASlots) & 1) ^ 1, pc[8], prof_on);  // MMA done with the slot
+#endif
+            tc_fence_after();
+            if (xa) tmem_st16(tA + 16 * xh, oa);
+            if (xb) tmem_st16(tA + 32 + 16 * xh, ob);
+#ifdef MXM_DEBUG_NAN
+            if (!s.i8 && ((xa && (bf2_nonfinite(sa) || bf2_nonfinite(za))) || (xb && (bf2_nonfinite(sb) || bf2_nonfinite(zb)))))
+              nan_note(p.prof, 1, t, ks, (int)(sa ^ (sb << 16)));
+#endif
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -872,17 +900,26 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const float sc = amax > 0.f ? __fdiv_rn(amax, fq) : 1.f;
           const uint4* src = reinterpret_cast<const uint4*>(p.H + row * p.f_max);
           uint2* dst = reinterpret_cast<uint2*>(p.Hq + row * p.f_max);
-          for (int i = lane; i < K / 8; i += 32) {
-            const uint4 v = __ldcg(src + i);
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-            uint32_t o[2] = {0, 0};
+          // kU 16-byte loads in flight per lane before any store (a single load per iteration leaves this pass
+          // latency-bound at a few GB/s per SM)
+          constexpr int kU = 8;
+          const int n8 = K / 8;
+          for (int i0 = lane; i0 < n8; i0 += 32 * kU) {
+            uint4 v[kU];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float x = bf16f((uint16_t)(w[e >> 1] >> (16 * (e & 1))));
-              const float qv = fminf(fmaxf(rintf(__fmul_rn(x, r)), -fq), fq);
-              o[e >> 2] |= ((uint32_t)(int)qv & 0xFFu) << (8 * (e & 3));
+            for (int u = 0; u < kU; ++u) v[u] = i0 + 32 * u < n8 ? __ldcg(src + i0 + 32 * u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+              uint32_t o[2] = {0, 0};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float x = bf16f((uint16_t)(w[e >> 1] >> (16 * (e & 1))));
+                const float qv = fminf(fmaxf(rintf(__fmul_rn(x, r)), -fq), fq);
+                o[e >> 2] |= ((uint32_t)(int)qv & 0xFFu) << (8 * (e & 3));
+              }
+              if (i0 + 32 * u < n8) dst[i0 + 32 * u] = make_uint2(o[0], o[1]);
             }
-            dst[i] = make_uint2(o[0], o[1]);
           }
           if (lane == 0) p.Hs[row] = sc;  // per-token: group 0 of the group-major [g][R] layout
         }
@@ -978,6 +1015,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               fa[j] = a2.x; fa[j + 1] = a2.y; fb[j] = b2.x; fb[j + 1] = b2.y;
             }
           }
+#ifdef MXM_DEBUG_NAN
+          for (int j = 0; j < 8; ++j)
+            if (c + j < nvalid && (!isfinite(fa[j]) || (two && !isfinite(fb[j]))))
+              nan_note(p.prof, t.phase == 0 ? 2 : 3, t, c + j, (int)__float_as_uint(isfinite(fa[j]) ? fb[j] : fa[j]));
+#endif
           if (t.phase == 0) {
             uint16_t hb[8];
 #pragma unroll
@@ -1066,10 +1108,12 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             const bool dst_hi = t.phase == 0 && nsl == 2 && si == 1;  // hetero: the up sub-loop
             const uint32_t aA = lane_addr + colA + (uint32_t)col0, aB = lane_addr + colB + (uint32_t)col0;
 #ifndef MXM_ABL_EPI
+            const unsigned long long t_dr = prof_on ? clock64() : 0ull;
             if (dst_hi)
               drain_event_any<16>(half, acc2, aA, aB, s.i8, false, s.g128, sw0, sw1, sa_ev);
             else
               drain_event_any<0>(half, acc2, aA, aB, s.i8, two, s.g128, sw0, sw1, sa_ev);
+            if (prof_on) pc[12] += clock64() - t_dr;  // register-accumulating drain time (diagnostic build)
 #endif
             tc_fence_before();
             __syncwarp();
@@ -1136,6 +1180,16 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   }
 }
 
+#ifdef MXM_DEBUG_NAN
+cudaError_t debug_nan_info(unsigned long long* out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_nan_info, sizeof(g_nan_info));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_nan_info, z, sizeof(z));
+  }
+  return e;
+}
+#endif
 cudaError_t launch_moe_gemm(const GemmParams& prm, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {

@@ -25,7 +25,7 @@ buf = torch.zeros(nsm, 16, dtype=torch.int64, device="cuda")
 L.debug_counters(buf); L(x, ids, w, sw); torch.cuda.synchronize(); L.debug_counters(None)
 c = buf.double().cpu().numpy(); tot = c[:, 15].mean()
 names = ["P ring", "P empty", "P dep", "M task", "M acce", "M full", "M aready", "X task", "X full", "E task",
-         "E accf", "M issue", "M subloop", "M stages", "E hq-dep", "total"]
+         "E accf", "M issue", "E drain", "M stages", "E hq-dep", "total"]
 print(f"{cfg.name} {tb} T={T}: kernel {tot:.0f} cycles (avg per CTA)")
 for i, n in enumerate(names):
     if n == "-": continue
