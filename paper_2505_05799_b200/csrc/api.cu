@@ -369,7 +369,7 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   // S4-S7 persistent group GEMM
   GemmParams prm;
   memset(&prm, 0, sizeof(prm));
-  const uint32_t boxes[4] = {16, 32, 64, 96};
+  const uint32_t boxes[4] = {16, 32, 64, MXM_DUAL_TILE};
   const void* srcs[5] = {P(w.Xb), P(w.XqA), P(w.XqB), P(w.H), P(w.Hq)};
   const bool isbf[5] = {true, false, false, true, false};
   const uint64_t cols[5] = {(uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->f_max, (uint64_t)l->f_max};

@@ -9,6 +9,10 @@
 namespace mxm {
 
 constexpr int kNumSms = 148;
+#ifndef MXM_ASLOTS
+#define MXM_ASLOTS 2  // TMEM A-ring depth of the group-GEMM (gemm.cu); sets the dual token tile below
+#endif
+#define MXM_DUAL_TILE (MXM_ASLOTS == 3 ? 80 : 96)  // max tokens of a dual (gate|up or paired-down) m-tile
 constexpr int kRowsPerTile = 128;  // output channels per tile (UMMA M)
 
 // Packed-format kinds (docs/packed_format.md)
@@ -73,12 +77,12 @@ struct Task {
 };
 static_assert(sizeof(Task) == 16, "task size");
 
-// Token-tile cap of an expert's m-tiles: dual gate/up tiles of up to 96 tokens fit one 192-column TMEM
-// accumulator buffer; register-accumulated tiles (g128 W-A dual, or gate and up as two sub-loops) keep
+// Token-tile cap of an expert's m-tiles: dual gate/up tiles of up to MXM_DUAL_TILE tokens fit one TMEM
+// accumulator buffer (2 x 160 columns next to a 3-slot A ring); register-accumulated tiles (g128 W-A dual, or gate and up as two sub-loops) keep
 // 64 columns per warpgroup half in registers -> 64 tokens.
 __host__ __device__ inline int tile_cap(const ExpertDesc& e) {
   const bool reg = !e.dual || (kind_is_i8(e.blk[0].geo.kind) && e.blk[0].geo.group == 128);
-  return reg ? 64 : 96;
+  return reg ? 64 : MXM_DUAL_TILE;
 }
 // Down tasks pair two 128-channel output tiles (two mats sharing the h tile) unless the down is a g128
 // W-A block whose register-accumulated drain would exceed 64 columns per thread.

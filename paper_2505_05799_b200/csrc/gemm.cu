@@ -33,11 +33,15 @@ constexpr int kRing = 4;
 // 128-channel down tiles) of up to 96 tokens fits one buffer, so every task is double-buffered against the
 // next one's MMAs -- and a 2-slot A ring at [384, 512) for TS-form MMAs (dequantized weights; per slot
 // 2 mats x 32 columns), decoupled from the 4 smem stages by its own ready / empty barriers.
+// MXM_ASLOTS=3 (2 x 160 accumulator columns, 80-token tiles, 3 A slots) was measured slower on every
+// config (DSV2 GEMM 0.93 -> 1.09 ms): the smaller tiles cost more than the deeper A ring saves.
 constexpr int kAccBufs = 2;
-constexpr int kAccCols = 192;
-constexpr int kMat1Col = 96;     // column offset of mat 1 inside an accumulator buffer
+constexpr int kASlots = MXM_ASLOTS;
+constexpr int kAccCols = kASlots == 3 ? 160 : 192;  // 2 x 160 + 3 x 64 = 2 x 192 + 2 x 64 = 512 columns
+constexpr int kMat1Col = kAccCols / 2;               // column offset of mat 1 inside an accumulator buffer
 constexpr int kTmemA = kAccBufs * kAccCols;
-constexpr int kASlots = 2;
+static_assert(kTmemA + 64 * kASlots == 512, "TMEM partition");
+static_assert(kMat1Col == MXM_DUAL_TILE, "dual token tile (common.cuh) must match the accumulator buffer");
 constexpr int kThreads = 640;  // 20 warps: producer, MMA issuer, 2 idle, 4 transform, 8 epilogue, 4 transform
 constexpr int kXfWarps = 8;     // transform warps 4..7 (K half 0) and 16..19 (K half 1); one A row per thread
 constexpr int kTileBytes = 16384;
@@ -113,7 +117,7 @@ __device__ __forceinline__ int build_subloops(const Task& t, const ExpertDesc* _
   return 1;
 }
 
-__device__ __forceinline__ int nt_index(int nt) { return nt <= 16 ? 0 : (nt <= 32 ? 1 : (nt <= 64 ? 2 : 3)); }
+__device__ __forceinline__ int nt_index(int nt) { return nt <= 16 ? 0 : (nt <= 32 ? 1 : (nt <= 64 ? 2 : 3)); }  // box 16/32/64/dual
 
 // activation scales of group g for rows [row0, row0 + nt): 16-byte-aligned source span and element offset
 __device__ __forceinline__ const float* ascale_span(const float* base, int64_t R, int g, int row0, uint32_t& off) {
@@ -150,6 +154,9 @@ __device__ __forceinline__ uint32_t bf2_fma(uint32_t a, uint32_t b, uint32_t c) 
 }
 // (128 + u_even, 128 + u_odd) as bf16x2 -> q*s + z rounded once to bf16 (q = u - off)
 __device__ __forceinline__ uint32_t deq_pair(uint32_t fields, uint32_t off2, uint32_t s2, uint32_t z2) {
+#ifdef MXM_ABL_XF_RAW  // timing diagnostic: raw (128 + u) codes, no scale / zero (numerically wrong)
+  return fields;
+#endif
   return bf2_fma(bf2_sub(fields, off2), s2, z2);
 }
 // codes of one pair at bits (sh, sh+16) of `word`, widths given by `mask`, as (128+u) bf16x2 (one LOP3)
@@ -263,24 +270,31 @@ __device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, int r,
   }
 }
 
-// one transform warpgroup's share (K half H) of one stage: both mats -> registers (oa, ob), stored to the TMEM A
-// ring by the caller once the MMA has released the slot (the unpack overlaps the MMAs still reading it)
+// one transform warpgroup's share (K half H) of one stage: both mats -> TMEM A ring (each mat's tcgen05.st
+// is issued as soon as it is unpacked, so it overlaps the next mat's unpack)
 template <int H>
-__device__ __forceinline__ void xform_stage(const SubLoop& s, const uint8_t* x0, const uint8_t* x1, int r, bool hmA,
-                                            bool hmB, int bitsA, int bitsB, int mbA, int mbB, bool symA, bool symB,
-                                            uint32_t offA, uint32_t offB, bool xa, bool xb, uint32_t& sa,
-                                            uint32_t& za, uint32_t& sb, uint32_t& zb, uint32_t (&oa)[16],
-                                            uint32_t (&ob)[16]) {
+__device__ __forceinline__ void xform_stage(const SubLoop& s, const uint8_t* x0, const uint8_t* x1, uint32_t tA, int r,
+                                            bool hmA, bool hmB, int bitsA, int bitsB, int mbA, int mbB, bool symA,
+                                            bool symB, uint32_t offA, uint32_t offB, bool xa, bool xb, uint32_t& sa,
+                                            uint32_t& za, uint32_t& sb, uint32_t& zb, uint32_t (&o)[16]) {
   if (s.i8) {
     if (xa) {
-      if (bitsA == 4) xform_wa<4, H>(x0, r, oa); else xform_wa<5, H>(x0, r, oa);
+      if (bitsA == 4) xform_wa<4, H>(x0, r, o); else xform_wa<5, H>(x0, r, o);
+      tmem_st16(tA + 16 * H, o);
     }
     if (xb) {
-      if (bitsB == 4) xform_wa<4, H>(x1, r, ob); else xform_wa<5, H>(x1, r, ob);
+      if (bitsB == 4) xform_wa<4, H>(x1, r, o); else xform_wa<5, H>(x1, r, o);
+      tmem_st16(tA + 32 + 16 * H, o);
     }
   } else {
-    if (xa) xform_wo_any<H>(bitsA, x0, hmA, mbA, symA, offA, r, sa, za, oa);
-    if (xb) xform_wo_any<H>(bitsB, x1, hmB, mbB, symB, offB, r, sb, zb, ob);
+    if (xa) {
+      xform_wo_any<H>(bitsA, x0, hmA, mbA, symA, offA, r, sa, za, o);
+      tmem_st16(tA + 16 * H, o);
+    }
+    if (xb) {
+      xform_wo_any<H>(bitsB, x1, hmB, mbB, symB, offB, r, sb, zb, o);
+      tmem_st16(tA + 32 + 16 * H, o);
+    }
   }
 }
 
@@ -328,13 +342,36 @@ template <int HALF, int DST0>
 __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8, bool two,
                                             bool small, float sw0, float sw1, const float* sa) {
   constexpr int CH = 8;  // 16-wide staging + 64 accumulators exceeds the 128-register epilogue budget (spills)
+  constexpr int NCH = HALF / CH;
   constexpr float kMagic = 12582912.f;  // 2^23 + 2^22
+  // software-pipelined: chunk c+1's TMEM loads are in flight while chunk c is scaled and accumulated
+  uint32_t va[2][CH], vb[2][CH];
 #pragma unroll
-  for (int c0 = 0; c0 < HALF; c0 += CH) {
-    uint32_t va[CH], vb[CH];
-    tmem_ld8(addrA + c0, va);
-    if (two) tmem_ld8(addrB + c0, vb);
-    tmem_ld_wait();
+  for (int j = 0; j < CH; ++j) vb[0][j] = vb[1][j] = 0u;
+#ifdef MXM_ABL_DRAIN_LD  // diagnostic: no TMEM loads (operands = lane-dependent constants)
+#define tmem_ld8(a, r) do { for (int _j = 0; _j < 8; ++_j) (r)[_j] = (a) + _j; } while (0)
+#define tmem_ld_wait_regs(a, b) do { } while (0)
+#endif
+  tmem_ld8(addrA, va[0]);
+  if (two) tmem_ld8(addrB, vb[0]);
+  tmem_ld_wait_regs(va[0], vb[0]);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int cur = c & 1;
+    if (c + 1 < NCH) {
+      tmem_ld8(addrA + (c + 1) * CH, va[cur ^ 1]);
+      if (two) tmem_ld8(addrB + (c + 1) * CH, vb[cur ^ 1]);
+    }
+    const int c0 = c * CH;
+#ifdef MXM_ABL_DRAIN_MATH  // diagnostic: loads only, one integer add per element
+    if (true) {
+#pragma unroll
+      for (int j = 0; j < CH; j += 2) {
+        const int col = c0 + j;
+        acc2[DST0 + col / 2].x = __int_as_float(__float_as_int(acc2[DST0 + col / 2].x) + (int)(va[cur][j] + vb[cur][j]));
+      }
+    } else
+#endif
     if (i8) {
 #pragma unroll
       for (int j = 0; j < CH; j += 2) {
@@ -345,13 +382,15 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
 #define MXM_MAGIC_I2F 0  // sm_100 converts with I2FP.F32.S32; the 2^23+2^22 add is an A/B alternative
 #endif
         if (MXM_MAGIC_I2F && small) {
-          fa = fadd2(make_float2(__int_as_float((int32_t)va[j] + 0x4B400000), __int_as_float((int32_t)va[j + 1] + 0x4B400000)),
+          fa = fadd2(make_float2(__int_as_float((int32_t)va[cur][j] + 0x4B400000),
+                                 __int_as_float((int32_t)va[cur][j + 1] + 0x4B400000)),
                      make_float2(-kMagic, -kMagic));
-          fb = fadd2(make_float2(__int_as_float((int32_t)vb[j] + 0x4B400000), __int_as_float((int32_t)vb[j + 1] + 0x4B400000)),
+          fb = fadd2(make_float2(__int_as_float((int32_t)vb[cur][j] + 0x4B400000),
+                                 __int_as_float((int32_t)vb[cur][j + 1] + 0x4B400000)),
                      make_float2(-kMagic, -kMagic));
         } else {
-          fa = make_float2((float)(int32_t)va[j], (float)(int32_t)va[j + 1]);
-          fb = make_float2((float)(int32_t)vb[j], (float)(int32_t)vb[j + 1]);
+          fa = make_float2((float)(int32_t)va[cur][j], (float)(int32_t)va[cur][j + 1]);
+          fb = make_float2((float)(int32_t)vb[cur][j], (float)(int32_t)vb[cur][j + 1]);
         }
         acc2[DST0 + col / 2] = ffma2(fa, fmul2(make_float2(sw0, sw0), sac), acc2[DST0 + col / 2]);
         if (two) acc2[16 + col / 2] = ffma2(fb, fmul2(make_float2(sw1, sw1), sac), acc2[16 + col / 2]);
@@ -360,12 +399,19 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
 #pragma unroll
       for (int j = 0; j < CH; j += 2) {
         const int col = c0 + j;
-        acc2[DST0 + col / 2] = fadd2(acc2[DST0 + col / 2], make_float2(__uint_as_float(va[j]), __uint_as_float(va[j + 1])));
+        acc2[DST0 + col / 2] =
+            fadd2(acc2[DST0 + col / 2], make_float2(__uint_as_float(va[cur][j]), __uint_as_float(va[cur][j + 1])));
         if (two)
-          acc2[16 + col / 2] = fadd2(acc2[16 + col / 2], make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1])));
+          acc2[16 + col / 2] =
+              fadd2(acc2[16 + col / 2], make_float2(__uint_as_float(vb[cur][j]), __uint_as_float(vb[cur][j + 1])));
       }
     }
+    if (c + 1 < NCH) tmem_ld_wait_regs(va[cur ^ 1], vb[cur ^ 1]);
   }
+#ifdef MXM_ABL_DRAIN_LD
+#undef tmem_ld8
+#undef tmem_ld_wait_regs
+#endif
 }
 
 template <int DST0>
@@ -380,6 +426,9 @@ __device__ __forceinline__ void drain_event_any(int half, float2 (&acc2)[32], ui
       break;
     case 32:
       drain_event<32, DST0>(acc2, addrA, addrB, i8, two, small, sw0, sw1, sa);
+      break;
+    case 40:  // single mat, 80-token tile
+      if constexpr (DST0 == 0) drain_event<40, 0>(acc2, addrA, addrB, i8, false, small, sw0, sw1, sa);
       break;
     case 48:  // single mat, 96-token tile
       if constexpr (DST0 == 0) drain_event<48, 0>(acc2, addrA, addrB, i8, false, small, sw0, sw1, sa);
@@ -454,7 +503,7 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned l
 }
 
 struct MmaState {
-  uint32_t stage, sphase, abuf, acc_ph, aidx;  // aidx: TS stages so far (A slot = aidx & 1)
+  uint32_t stage, sphase, abuf, acc_ph, aidx;  // aidx: TS stages so far (A slot = aidx % kASlots)
 };
 
 // One sub-loop of MMAs (all K stages of one or two mats sharing the token tile), specialised on the MMA
@@ -494,7 +543,7 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
     const uint32_t d0 = tmem + b0 * (uint32_t)kAccCols;
     const uint32_t d1 = d0 + (uint32_t)kMat1Col;
     const uint32_t blo = lo0 + stage * kSlotLo;
-    const uint32_t aslot = st.aidx & (kASlots - 1);
+    const uint32_t aslot = st.aidx % kASlots;
     const uint32_t at0 = tmem + kTmemA + aslot * 64u;
     // one wait per stage: a TS stage's A slot is ready only after the transform saw the stage's data
     if (any_ts) {
@@ -530,6 +579,9 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
           }
         }
       }
+      // TS stage: the transform warps finished reading the smem stage before aready, so the MMA thread
+      // arrives for them on the stage's empty barrier (they arrive themselves only on weight-image stages)
+      if (any_ts) mbar_arrive_cnt(&ctl.empty[stage], kXfWarps);
       mma_commit(&ctl.empty[stage]);
       if (any_ts) mma_commit(&ctl.aempty[aslot]);
       if (ev_end) mma_commit(&ctl.accf[b0]);
@@ -809,40 +861,32 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const bool hmA = gca == 0, hmB = gcb == 0;
           if (++gca == gstA) gca = 0;
           if (++gcb == gstB) gcb = 0;
-          twait(&ctl.full[stage], sphase, pc[8], prof_on);
           if (!s.xform) {
+            twait(&ctl.full[stage], sphase, pc[8], prof_on);
             __syncwarp();
             if (MXM_EMPTY_XF && lane == 0) mbar_arrive(&ctl.empty[stage]);
           } else {
-            const uint32_t aslot = aidx & (kASlots - 1);
-#ifndef MXM_XF_EARLY
-#define MXM_XF_EARLY 1  // 1: unpack before waiting for the A slot (overlaps the MMAs still reading it)
-#endif
-#if !MXM_XF_EARLY
-            twait(&ctl.aempty[aslot], ((aidx / kASlots) & 1) ^ 1, pc[8], prof_on);
-#endif
-            // dequantized / unpacked rows go to the TMEM A ring (lane = row); one tcgen05.st per mat and K half
+            const uint32_t aslot = aidx % kASlots;
+            twait(&ctl.aempty[aslot], ((aidx / kASlots) & 1) ^ 1, pc[8], prof_on);  // MMA done with the slot
+            twait(&ctl.full[stage], sphase, pc[8], prof_on);
+            tc_fence_after();
+            // dequantized / unpacked rows go to the TMEM A ring (lane = row); one tcgen05.st per mat and K half,
+            // mat 0's store in flight while mat 1 is unpacked
             const uint32_t tA = tmem + ((uint32_t)(r & ~31) << 16) + kTmemA + aslot * 64u;
-            uint32_t oa[16], ob[16];
+            uint32_t o[16];
 #ifdef MXM_ABL_XFORM
 #pragma unroll
-            for (int i = 0; i < 16; ++i) oa[i] = ob[i] = 0x3f803f80u;
+            for (int i = 0; i < 16; ++i) o[i] = 0x3f803f80u;
+            tmem_st16(tA + 16 * xh, o);
+            if (two) tmem_st16(tA + 32 + 16 * xh, o);
             if (0)
 #endif
             if (xh)
-              xform_stage<1>(s, tileX(stage, 0), tileX(stage, 1), r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
-                             offA, offB, xa, xb, sa, za, sb, zb, oa, ob);
+              xform_stage<1>(s, tileX(stage, 0), tileX(stage, 1), tA, r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
+                             offA, offB, xa, xb, sa, za, sb, zb, o);
             else
-              xform_stage<0>(s, tileX(stage, 0), tileX(stage, 1), r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
-                             offA, offB, xa, xb, sa, za, sb, zb, oa, ob);
-            __syncwarp();
-            if (MXM_EMPTY_XF && lane == 0) mbar_arrive(&ctl.empty[stage]);  // this warp's smem reads are done
-#if MXM_XF_EARLY
-            twait(&ctl.aempty[aslot], ((aidx / kASlots) & 1) ^ 1, pc[8], prof_on);  // MMA done with the slot
-#endif
-            tc_fence_after();
-            if (xa) tmem_st16(tA + 16 * xh, oa);
-            if (xb) tmem_st16(tA + 32 + 16 * xh, ob);
+              xform_stage<0>(s, tileX(stage, 0), tileX(stage, 1), tA, r, hmA, hmB, bitsA, bitsB, mbA, mbB, symA, symB,
+                             offA, offB, xa, xb, sa, za, sb, zb, o);
 #ifdef MXM_DEBUG_NAN
             if (!s.i8 && ((xa && (bf2_nonfinite(sa) || bf2_nonfinite(za))) || (xb && (bf2_nonfinite(sb) || bf2_nonfinite(zb)))))
               nan_note(p.prof, 1, t, ks, (int)(sa ^ (sb << 16)));

@@ -45,9 +45,9 @@ __device__ int block_excl_scan(int v, int* warp_tot, int* out_total) {
   return base + x - v;
 }
 
-// token tile of an m-tile with m rows: 16 / 32 / 64 / 96 (the TMA boxes, MMA N)
+// token tile of an m-tile with m rows: 16 / 32 / 64 / MXM_DUAL_TILE (the TMA boxes, MMA N)
 __device__ __forceinline__ int pow2_tile(int m) {
-  return m <= 16 ? 16 : (m <= 32 ? 32 : (m <= 64 ? 64 : 96));
+  return m <= 16 ? 16 : (m <= 32 ? 32 : (m <= 64 ? 64 : MXM_DUAL_TILE));
 }
 
 __device__ __forceinline__ float tile_cost(const ExpertDesc& e, int d, int nt) {
