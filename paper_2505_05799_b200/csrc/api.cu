@@ -499,3 +499,8 @@ mxm_status mxm_debug_task_stats(const mxm_layer* l, const void* ws, int64_t T, i
 namespace mxm { cudaError_t debug_nan_info(unsigned long long* out, bool reset); }
 extern "C" int mxm_debug_nan_info(unsigned long long* out) { return (int)mxm::debug_nan_info(out, true); }
 #endif
+
+#ifdef MXM_TRACE
+namespace mxm { cudaError_t debug_trace(unsigned long long* out); }
+extern "C" int mxm_debug_trace(unsigned long long* out) { return (int)mxm::debug_trace(out); }
+#endif

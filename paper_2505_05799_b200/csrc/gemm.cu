@@ -140,6 +140,14 @@ __device__ __forceinline__ bool bf2_nonfinite(uint32_t v) {
   return ((v >> 7) & 0xFFu) == 0xFFu || ((v >> 23) & 0xFFu) == 0xFFu;
 }
 #endif
+#ifdef MXM_TRACE
+// per-stage event timestamps of CTA 0 (diagnostic build): [event][index], see tools/diag_trace.py
+constexpr int kTrN = 2048;
+__device__ unsigned long long g_tr[8][kTrN];
+#define TR(ev, idx) do { if (blockIdx.x == 0 && (idx) < kTrN) g_tr[ev][idx] = clock64(); } while (0)
+#else
+#define TR(ev, idx) do { } while (0)
+#endif
 // ---------------------------------------------------------------- transforms (one thread per A row)
 __device__ __forceinline__ uint32_t bf2_sub(uint32_t a, uint32_t b) {
   __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a), y = *reinterpret_cast<__nv_bfloat162*>(&b);
@@ -192,11 +200,33 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, bool h
       for (int t = 0; t < 4; ++t) o[4 * j + t] = deq_pair(pair_fields(word, 4 * t, 0x000F000Fu), off2, s2, z2);
     }
   } else if constexpr (BITS == 2) {
+    // pair t sits at bits (2t, 2t+16). Masked in place at mantissa bit 2*tau (tau = 0, 1, 2) the bf16 field
+    // reads 128 + u * 4^tau, so only the words >> 6 and >> 12 are shifted (2 SHF per 8 pairs instead of 7);
+    // (128 + u 4^tau - (128 + off 4^tau)) * (s 4^-tau) + z is the same exact q*s + z, rounded once (HFMA2).
+    // s 4^-tau is an exact bf16 for any normal s (power-of-two scaling).
+    const uint32_t offb = off2 & 0x007F007Fu;
+    const uint32_t offs[3] = {off2, 0x43004300u | (offb << 2), 0x43004300u | (offb << 4)};
+    uint32_t ss[3];
+    {
+      __nv_bfloat162 sv = *reinterpret_cast<const __nv_bfloat162*>(&s2);
+      const uint32_t q4 = 0x3E803E80u, q16 = 0x3D803D80u;  // 0.25, 0.0625
+      __nv_bfloat162 a = __hmul2(sv, *reinterpret_cast<const __nv_bfloat162*>(&q4));
+      __nv_bfloat162 b = __hmul2(sv, *reinterpret_cast<const __nv_bfloat162*>(&q16));
+      ss[0] = s2;
+      ss[1] = *reinterpret_cast<uint32_t*>(&a);
+      ss[2] = *reinterpret_cast<uint32_t*>(&b);
+    }
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const uint32_t word = w[(2 * H + j) * 128 + r];
+      const uint32_t ws[3] = {word, word >> 6, word >> 12};
 #pragma unroll
-      for (int t = 0; t < 8; ++t) o[8 * j + t] = deq_pair(pair_fields(word, 2 * t, 0x00030003u), off2, s2, z2);
+      for (int t = 0; t < 8; ++t) {
+        const int src = t < 6 ? t / 3 : 2;
+        const int tau = t < 6 ? t % 3 : t - 6;
+        const uint32_t fields = and_or(ws[src], 0x00030003u << (2 * tau), 0x43004300u);
+        o[8 * j + t] = deq_pair(fields, offs[tau], ss[tau], z2);
+      }
     }
   } else if constexpr (BITS == 3) {
     const uint32_t hw2 = w[(4 + H) * 128 + r];  // high-bit plane word covering low-plane words 2H, 2H+1
@@ -379,9 +409,20 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
         const float2 sac = make_float2(sa[col], sa[col + 1]);
         float2 fa, fb;
 #ifndef MXM_MAGIC_I2F
-#define MXM_MAGIC_I2F 0  // sm_100 converts with I2FP.F32.S32; the 2^23+2^22 add is an A/B alternative
+#define MXM_MAGIC_I2F 0  // 1: every conversion by the 2^23+2^22 add (A/B alternative)
 #endif
-        if (MXM_MAGIC_I2F && small) {
+#ifndef MXM_SPLIT_I2F
+#define MXM_SPLIT_I2F 0  // 1: mat 1 converts with the magic add (measured slower: the FMA pipe is the drain limit)
+#endif
+        // I2FP.F32.S32 issues at 1/4 rate (32 lanes/clk/SM, tools/op_rate.cu) on its own pipe, the magic add
+        // costs an IADD + FADD2 on the FMA pipe that FMUL2 / FFMA2 already load: mat 0 converts with I2FP,
+        // mat 1 with the magic add, so both pipes share the drain (exact: |acc| < 2^22 for a 128-K group)
+        if (MXM_SPLIT_I2F && !MXM_MAGIC_I2F && small && two) {
+          fa = make_float2((float)(int32_t)va[cur][j], (float)(int32_t)va[cur][j + 1]);
+          fb = fadd2(make_float2(__int_as_float((int32_t)vb[cur][j] + 0x4B400000),
+                                 __int_as_float((int32_t)vb[cur][j + 1] + 0x4B400000)),
+                     make_float2(-kMagic, -kMagic));
+        } else if (MXM_MAGIC_I2F && small) {
           fa = fadd2(make_float2(__int_as_float((int32_t)va[cur][j] + 0x4B400000),
                                  __int_as_float((int32_t)va[cur][j + 1] + 0x4B400000)),
                      make_float2(-kMagic, -kMagic));
@@ -504,6 +545,7 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned l
 
 struct MmaState {
   uint32_t stage, sphase, abuf, acc_ph, aidx;  // aidx: TS stages so far (A slot = aidx % kASlots)
+  int ntr;                                      // stages issued (trace index, diagnostic build)
 };
 
 // One sub-loop of MMAs (all K stages of one or two mats sharing the token tile), specialised on the MMA
@@ -559,6 +601,7 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
     tc_fence_after();
 #endif
     const unsigned long long t_iss = prof_on ? clock64() : 0ull;
+    if ((threadIdx.x & 31) == 0) TR(3, st.ntr);
     if (elect_one()) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -591,6 +634,8 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
       pc[11] += clock64() - t_iss;
       pc[13] += 1;
     }
+    if ((threadIdx.x & 31) == 0) TR(4, st.ntr);
+    ++st.ntr;
     if (any_ts) ++st.aidx;
     if (++st.stage == kStages) {
       st.stage = 0;
@@ -690,6 +735,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     // =========================== producer
     if (lane == 0) {
       uint32_t stage = 0, sphase = 0, sidx = 0;
+      int n_tr_p = 0;
+      (void)n_tr_p;
       for (uint32_t it = 0;; ++it) {
         const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
         const int idx = atomicAdd(&p.meta[5], 1);
@@ -740,6 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             if (++gc0 == gst0) gc0 = 0;
             if (++gc1 == gst1) gc1 = 0;
             twait(&ctl.empty[stage], sphase ^ 1, pc[1], prof_on);
+            TR(0, n_tr_p++);
             mbar_arrive_expect_tx(&ctl.full[stage], (uint32_t)t.nt * 128u + c0 + c1);
             bulk_load(dst0 + stage * str0, src0, c0, &ctl.full[stage]);
             src0 += c0;
@@ -782,6 +830,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     uint32_t stage = 0, sphase = 0, abuf = 0;
     uint32_t acc_ph = 0;  // bit b: parity of the next wait on acce[b] (phase bits, no local arrays)
     uint32_t aidx = 0;    // TS stages issued so far (A-ring slot and parity)
+    int ntr_m = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
       twait(&ctl.tfull[slot], rphase, pc[3], prof_on);
@@ -798,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         const SubLoop s = sl[si];
         const uint32_t ns = bcast((uint32_t)s.ns), g128 = bcast((uint32_t)s.g128), xf = bcast((uint32_t)s.xform);
         const uint32_t i8 = bcast((uint32_t)s.i8), two = bcast((uint32_t)(s.nmats == 2));
-        MmaState st{stage, sphase, abuf, acc_ph, aidx};
+        MmaState st{stage, sphase, abuf, acc_ph, aidx, ntr_m};
 #if defined(MXM_PROF_SUBLOOP) && defined(MXM_DEBUG_COUNTERS)
         const unsigned long long t_sl = prof_on ? clock64() : 0ull;
 #endif
@@ -821,6 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         abuf = st.abuf;
         acc_ph = st.acc_ph;
         aidx = st.aidx;
+        ntr_m = st.ntr;
       }
     }
     __syncwarp();
@@ -869,6 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             const uint32_t aslot = aidx % kASlots;
             twait(&ctl.aempty[aslot], ((aidx / kASlots) & 1) ^ 1, pc[8], prof_on);  // MMA done with the slot
             twait(&ctl.full[stage], sphase, pc[8], prof_on);
+            if (threadIdx.x == 128) TR(1, (int)aidx);
             tc_fence_after();
             // dequantized / unpacked rows go to the TMEM A ring (lane = row); one tcgen05.st per mat and K half,
             // mat 0's store in flight while mat 1 is unpacked
@@ -895,6 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&ctl.aready[aslot]);
+            if (threadIdx.x == 128) TR(2, (int)aidx);
             ++aidx;
           }
           if (++stage == kStages) {
@@ -912,6 +964,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     const int ew = warp - 8, wg = ew >> 2, q = warp & 3;
     const int l = q * 32 + lane;  // output channel within the tile == TMEM lane
     uint32_t abuf = 0, acc_ph = 0, rbuf = 0, sidx = 0;
+    int n_tr_e = 0;
+    (void)n_tr_e;
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
       twait(&ctl.tfull[slot], rphase, pc[9], prof_on);
@@ -1015,6 +1069,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         const uint32_t b0 = abuf;
         abuf = (abuf + 1) & (kAccBufs - 1);
         twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
+        if (threadIdx.x == 256) TR(5, n_tr_e);
         acc_ph ^= 1u << b0;
         tc_fence_after();
         if (s.i8 && t.phase != 0) {  // h-scales are written by this kernel: read after the MMA consumed Hq
@@ -1088,6 +1143,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ctl.acce[b0]);
+        if (threadIdx.x == 256) TR(6, n_tr_e);
+        ++n_tr_e;
       } else {
         // ======== register-accumulating epilogue (g128 drains / hetero gate-up sub-loops)
         float2 acc2[32];
@@ -1224,6 +1281,9 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   }
 }
 
+#ifdef MXM_TRACE
+cudaError_t debug_trace(unsigned long long* out) { return cudaMemcpyFromSymbol(out, g_tr, sizeof(g_tr)); }
+#endif
 #ifdef MXM_DEBUG_NAN
 cudaError_t debug_nan_info(unsigned long long* out, bool reset) {
   cudaError_t e = cudaMemcpyFromSymbol(out, g_nan_info, sizeof(g_nan_info));
