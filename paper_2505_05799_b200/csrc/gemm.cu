@@ -19,6 +19,7 @@
 // group"), ping-ponging between TMEM buffers so the tensor core keeps running.
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "actq.cuh"
 #include "common.cuh"
@@ -368,9 +369,11 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // `sa` is this warp's smem copy of the event's activation scales (broadcast reads, no shuffles).
 // SMALL (g128 groups: |int32| <= 128*127*127 < 2^22): exact int->float by the 2^23+2^22 magic add
 // (IADD + FADD on the full-rate pipes instead of the quarter-rate I2F).
-template <int HALF, int DST0>
-__device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8, bool two,
-                                            bool small, float sw0, float sw1, const float* sa) {
+// I8 / TWO / SMALL are template parameters: with run-time flags the compiler if-converts both conversion
+// paths and the mat-1 work into predicated instructions that still take issue slots
+template <int HALF, int DST0, bool I8, bool TWO, bool SMALL>
+__device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, float sw0, float sw1,
+                                            const float* sa) {
   constexpr int CH = 8;  // 16-wide staging + 64 accumulators exceeds the 128-register epilogue budget (spills)
   constexpr int NCH = HALF / CH;
   constexpr float kMagic = 12582912.f;  // 2^23 + 2^22
@@ -383,14 +386,14 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
 #define tmem_ld_wait_regs(a, b) do { } while (0)
 #endif
   tmem_ld8(addrA, va[0]);
-  if (two) tmem_ld8(addrB, vb[0]);
+  if constexpr (TWO) tmem_ld8(addrB, vb[0]);
   tmem_ld_wait_regs(va[0], vb[0]);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int cur = c & 1;
     if (c + 1 < NCH) {
       tmem_ld8(addrA + (c + 1) * CH, va[cur ^ 1]);
-      if (two) tmem_ld8(addrB + (c + 1) * CH, vb[cur ^ 1]);
+      if constexpr (TWO) tmem_ld8(addrB + (c + 1) * CH, vb[cur ^ 1]);
     }
     const int c0 = c * CH;
 #ifdef MXM_ABL_DRAIN_MATH  // diagnostic: loads only, one integer add per element
@@ -402,7 +405,7 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
       }
     } else
 #endif
-    if (i8) {
+    if constexpr (I8) {
 #pragma unroll
       for (int j = 0; j < CH; j += 2) {
         const int col = c0 + j;
@@ -417,12 +420,12 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
         // I2FP.F32.S32 issues at 1/4 rate (32 lanes/clk/SM, tools/op_rate.cu) on its own pipe, the magic add
         // costs an IADD + FADD2 on the FMA pipe that FMUL2 / FFMA2 already load: mat 0 converts with I2FP,
         // mat 1 with the magic add, so both pipes share the drain (exact: |acc| < 2^22 for a 128-K group)
-        if (MXM_SPLIT_I2F && !MXM_MAGIC_I2F && small && two) {
+        if constexpr (MXM_SPLIT_I2F && !MXM_MAGIC_I2F && SMALL && TWO) {
           fa = make_float2((float)(int32_t)va[cur][j], (float)(int32_t)va[cur][j + 1]);
           fb = fadd2(make_float2(__int_as_float((int32_t)vb[cur][j] + 0x4B400000),
                                  __int_as_float((int32_t)vb[cur][j + 1] + 0x4B400000)),
                      make_float2(-kMagic, -kMagic));
-        } else if (MXM_MAGIC_I2F && small) {
+        } else if constexpr (MXM_MAGIC_I2F && SMALL) {
           fa = fadd2(make_float2(__int_as_float((int32_t)va[cur][j] + 0x4B400000),
                                  __int_as_float((int32_t)va[cur][j + 1] + 0x4B400000)),
                      make_float2(-kMagic, -kMagic));
@@ -434,7 +437,7 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
           fb = make_float2((float)(int32_t)vb[cur][j], (float)(int32_t)vb[cur][j + 1]);
         }
         acc2[DST0 + col / 2] = ffma2(fa, fmul2(make_float2(sw0, sw0), sac), acc2[DST0 + col / 2]);
-        if (two) acc2[16 + col / 2] = ffma2(fb, fmul2(make_float2(sw1, sw1), sac), acc2[16 + col / 2]);
+        if constexpr (TWO) acc2[16 + col / 2] = ffma2(fb, fmul2(make_float2(sw1, sw1), sac), acc2[16 + col / 2]);
       }
     } else {
 #pragma unroll
@@ -442,7 +445,7 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
         const int col = c0 + j;
         acc2[DST0 + col / 2] =
             fadd2(acc2[DST0 + col / 2], make_float2(__uint_as_float(va[cur][j]), __uint_as_float(va[cur][j + 1])));
-        if (two)
+        if constexpr (TWO)
           acc2[16 + col / 2] =
               fadd2(acc2[16 + col / 2], make_float2(__uint_as_float(vb[cur][j]), __uint_as_float(vb[cur][j + 1])));
       }
@@ -455,28 +458,42 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
 #endif
 }
 
+template <int DST0, bool I8, bool TWO, bool SMALL>
+__device__ __forceinline__ void drain_half(int half, float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, float sw0,
+                                           float sw1, const float* sa) {
+  // two mats: tiles of <= 64 tokens (half <= 32). One mat: also a g128 W-A down of an expert whose gate/up
+  // allow 96-token tiles (single-mat down, half 48); half 64 keeps the 128-token case total
+  if (half == 8) {
+    drain_event<8, DST0, I8, TWO, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+  } else if (half == 16) {
+    drain_event<16, DST0, I8, TWO, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+  } else if (half == 32 || TWO || DST0 != 0) {
+    drain_event<32, DST0, I8, TWO, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+  } else if constexpr (!TWO && DST0 == 0) {
+    if (half == 40)
+      drain_event<40, 0, I8, false, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+    else if (half == 48)
+      drain_event<48, 0, I8, false, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+    else
+      drain_event<64, 0, I8, false, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+  }
+}
+
+// i8 && small: W-A g128 events (dual or single mat); i8 && !small / bf16: one mat of a heterogeneous
+// gate/up pair (never two mats)
 template <int DST0>
 __device__ __forceinline__ void drain_event_any(int half, float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8,
                                                 bool two, bool small, float sw0, float sw1, const float* sa) {
-  switch (half) {
-    case 8:
-      drain_event<8, DST0>(acc2, addrA, addrB, i8, two, small, sw0, sw1, sa);
-      break;
-    case 16:
-      drain_event<16, DST0>(acc2, addrA, addrB, i8, two, small, sw0, sw1, sa);
-      break;
-    case 32:
-      drain_event<32, DST0>(acc2, addrA, addrB, i8, two, small, sw0, sw1, sa);
-      break;
-    case 40:  // single mat, 80-token tile
-      if constexpr (DST0 == 0) drain_event<40, 0>(acc2, addrA, addrB, i8, false, small, sw0, sw1, sa);
-      break;
-    case 48:  // single mat, 96-token tile
-      if constexpr (DST0 == 0) drain_event<48, 0>(acc2, addrA, addrB, i8, false, small, sw0, sw1, sa);
-      break;
-    default:
-      if constexpr (DST0 == 0) drain_event<64, 0>(acc2, addrA, addrB, i8, false, small, sw0, sw1, sa);
-      break;
+  if (i8 && small) {
+    if (two) {
+      if constexpr (DST0 == 0) drain_half<0, true, true, true>(half, acc2, addrA, addrB, sw0, sw1, sa);
+    } else {
+      drain_half<DST0, true, false, true>(half, acc2, addrA, addrB, sw0, sw1, sa);
+    }
+  } else if (i8) {
+    drain_half<DST0, true, false, false>(half, acc2, addrA, addrB, sw0, sw1, sa);
+  } else {
+    drain_half<DST0, false, false, false>(half, acc2, addrA, addrB, sw0, sw1, sa);
   }
 }
 
@@ -787,7 +804,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             if (++gc0 == gst0) gc0 = 0;
             if (++gc1 == gst1) gc1 = 0;
             twait(&ctl.empty[stage], sphase ^ 1, pc[1], prof_on);
-            TR(0, n_tr_p++);
+            TR(0, n_tr_p);
+            ++n_tr_p;
             mbar_arrive_expect_tx(&ctl.full[stage], (uint32_t)t.nt * 128u + c0 + c1);
             bulk_load(dst0 + stage * str0, src0, c0, &ctl.full[stage]);
             src0 += c0;
@@ -1089,20 +1107,23 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         const uint32_t colB = colA + (uint32_t)kMat1Col;
         const float2 swa = make_float2(sw0, sw0), swb = make_float2(sw1, sw1);
 #ifndef MXM_ABL_EPI
+        // specialised on (W-A, two mats, phase 0): with run-time flags the compiler predicates both variants
+        auto stream = [&](auto i8_c, auto two_c, auto p0_c) {
+        constexpr bool I8 = decltype(i8_c)::value, TWO = decltype(two_c)::value, P0 = decltype(p0_c)::value;
 #pragma unroll 1
         for (int c = 0; c < half; c += 8) {
           uint32_t va[8], vb[8];
           const uint32_t cbase = (uint32_t)(col0 + c);
           tmem_ld8(lane_addr + colA + cbase, va);
-          if (two) tmem_ld8(lane_addr + colB + cbase, vb);
+          if constexpr (TWO) tmem_ld8(lane_addr + colB + cbase, vb);
           tmem_ld_wait();
           float fa[8], fb[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             fa[j] = __uint_as_float(va[j]);
-            fb[j] = __uint_as_float(vb[j]);
+            fb[j] = TWO ? __uint_as_float(vb[j]) : 0.f;
           }
-          if (s.i8) {  // per-column activation scale: broadcast smem reads
+          if constexpr (I8) {  // per-column activation scale: broadcast smem reads
             const float4 x0 = *reinterpret_cast<const float4*>(cw_sa + c);
             const float4 x1 = *reinterpret_cast<const float4*>(cw_sa + c + 4);
             const float2 s2[4] = {make_float2(x0.x, x0.y), make_float2(x0.z, x0.w), make_float2(x1.x, x1.y),
@@ -1110,16 +1131,20 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 #pragma unroll
             for (int j = 0; j < 8; j += 2) {
               const float2 a2 = fmul2(make_float2((float)(int32_t)va[j], (float)(int32_t)va[j + 1]), fmul2(swa, s2[j / 2]));
-              const float2 b2 = fmul2(make_float2((float)(int32_t)vb[j], (float)(int32_t)vb[j + 1]), fmul2(swb, s2[j / 2]));
-              fa[j] = a2.x; fa[j + 1] = a2.y; fb[j] = b2.x; fb[j + 1] = b2.y;
+              fa[j] = a2.x; fa[j + 1] = a2.y;
+              if constexpr (TWO) {
+                const float2 b2 =
+                    fmul2(make_float2((float)(int32_t)vb[j], (float)(int32_t)vb[j + 1]), fmul2(swb, s2[j / 2]));
+                fb[j] = b2.x; fb[j + 1] = b2.y;
+              }
             }
           }
 #ifdef MXM_DEBUG_NAN
           for (int j = 0; j < 8; ++j)
-            if (c + j < nvalid && (!isfinite(fa[j]) || (two && !isfinite(fb[j]))))
+            if (c + j < nvalid && (!isfinite(fa[j]) || (TWO && !isfinite(fb[j]))))
               nan_note(p.prof, t.phase == 0 ? 2 : 3, t, c + j, (int)__float_as_uint(isfinite(fa[j]) ? fb[j] : fa[j]));
 #endif
-          if (t.phase == 0) {
+          if constexpr (P0) {
             uint16_t hb[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) hb[j] = f2bf(silu_f(fa[j]) * fb[j]);
@@ -1134,10 +1159,20 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             for (int j = 0; j < 8; ++j) {
               if (c + j < nvalid) {
                 o0[(int64_t)j * p.d] = f2bf(fa[j] * rw[j]);
-                if (two) o1[(int64_t)j * p.d] = f2bf(fb[j] * rw[j]);
+                if constexpr (TWO) o1[(int64_t)j * p.d] = f2bf(fb[j] * rw[j]);
               }
             }
           }
+        }
+        };
+        using Tt = std::true_type;
+        using Ft = std::false_type;
+        if (t.phase == 0) {
+          if (s.i8) { if (two) stream(Tt{}, Tt{}, Tt{}); else stream(Tt{}, Ft{}, Tt{}); }
+          else { if (two) stream(Ft{}, Tt{}, Tt{}); else stream(Ft{}, Ft{}, Tt{}); }
+        } else {
+          if (s.i8) { if (two) stream(Tt{}, Tt{}, Ft{}); else stream(Tt{}, Ft{}, Ft{}); }
+          else { if (two) stream(Ft{}, Tt{}, Ft{}); else stream(Ft{}, Ft{}, Ft{}); }
         }
 #endif
         tc_fence_before();

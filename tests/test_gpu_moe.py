@@ -107,3 +107,13 @@ def test_q15_table6_mix(mx):
     rows = np.arange(0, 512, 8)
     e, _, _ = _parity(case, rows=rows)
     assert e <= TOL, e
+
+
+def test_wide_tile_single_mat_g128_down(mx):
+    """Gate/up per-channel W-A (96-token dual tiles) with a g128 W-A down: the down runs single-mat on a
+    96-token tile and drains 48 columns per warpgroup every 128-K group (regression: half-48 drains)."""
+    pc, g = C.WA(8, -1), C.WA(4, 128)
+    table = [[pc, pc, g], [pc, pc, C.WA(8, 128)], [pc, pc, g], [C.WO(4, 128), C.WO(4, 128), g]]
+    case = make_case(TINY, table, 300, seed=9)
+    e, _, _ = _parity(case)
+    assert e <= TOL, e
