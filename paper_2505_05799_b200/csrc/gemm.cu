@@ -409,7 +409,8 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
 #pragma unroll
       for (int j = 0; j < CH; j += 2) {
         const int col = c0 + j;
-        const float2 sac = make_float2(sa[col], sa[col + 1]);
+        const float4 sa4 = *reinterpret_cast<const float4*>(sa + (col & ~3));  // 16-B aligned, broadcast
+        const float2 sac = (col & 2) ? make_float2(sa4.z, sa4.w) : make_float2(sa4.x, sa4.y);
         float2 fa, fb;
 #ifndef MXM_MAGIC_I2F
 #define MXM_MAGIC_I2F 0  // 1: every conversion by the 2^23+2^22 add (A/B alternative)
@@ -1226,7 +1227,13 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               if (two) sw1 = bf16f(reinterpret_cast<const uint16_t*>(slotp + 256)[l]);
               uint32_t aoff;
               (void)ascale_span(xs_s, gs, ev, t.row0, aoff);
-              sa_ev = reinterpret_cast<const float*>(slotp + 512) + aoff + col0;
+              // restage this warp's column scales 16-byte aligned (drain reads them as broadcast float4s)
+              const float* src = reinterpret_cast<const float*>(slotp + 512) + aoff + col0;
+              __syncwarp();
+              cw_sa[lane] = lane < half ? src[lane] : 0.f;
+              if (half > 32) cw_sa[32 + lane] = 32 + lane < half ? src[32 + lane] : 0.f;
+              __syncwarp();
+              sa_ev = cw_sa;
             } else if (s.i8) {
               if (!pre) {  // h-scales are written by this kernel: read after the MMA consumed Hq (ld.cg)
                 sw0 = bf16f(__ldg(wsc0 + n));
