@@ -4,7 +4,7 @@ mkdir -p gpurun_out/final
 timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/final/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/final/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/final/smoke.log
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_throttle_reasons.active --format=csv > gpurun_out/final/smi.txt 2>&1
-timeout 900 python bench.py > gpurun_out/final/bench_dsv2.json 2> gpurun_out/final/bench_dsv2.err
+timeout 900 python bench.py --cpu-sample 128 > gpurun_out/final/bench_dsv2.json 2> gpurun_out/final/bench_dsv2.err
 for c in q15 mx q2; do
   timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/final/bench_$c.json 2> gpurun_out/final/bench_$c.err
 done
