@@ -85,8 +85,16 @@ struct mxm_layer {
   void* prof_counters = nullptr;  // device [grid][16] u64 wait-site cycle counters (debug)
   int64_t prof_calls = 0;
   std::vector<cudaEvent_t> prof_ev;
+  // S3 (plan) depends only on S1's offsets, so it runs on a side stream concurrently with S2 (gather):
+  // fork / join with events on the caller's stream (graph-capturable); created on first use
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::mutex side_mu;  // the fork / join events are per layer: concurrent calls serialise this section
   ~mxm_layer() {
     for (auto e : prof_ev) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
   }
 };
 static constexpr int kProfEv = 6;  // start | route | gather | plan | gemm | combine
@@ -357,15 +365,26 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   MXM_CUDA(launch_route_prep(topk_ids, topk_w, T, k, l->E, l->S, shared_w, (int32_t*)P(w.counts), nullptr, v_off,
                              nullptr, row_src, row_w, row_exp, inv, err, P(w.route_scratch), st));
   mark(1);
+  // S3 plan on the side stream (needs only S1's offsets), concurrent with S2 on the caller's stream
+  mxm_layer* ml = const_cast<mxm_layer*>(l);
+  std::lock_guard<std::mutex> side_lock(ml->side_mu);
+  if (!ml->side) {
+    MXM_CUDA(cudaStreamCreateWithFlags(&ml->side, cudaStreamNonBlocking));
+    MXM_CUDA(cudaEventCreateWithFlags(&ml->ev_fork, cudaEventDisableTiming));
+    MXM_CUDA(cudaEventCreateWithFlags(&ml->ev_join, cudaEventDisableTiming));
+  }
+  MXM_CUDA(cudaEventRecord(ml->ev_fork, st));
+  MXM_CUDA(cudaStreamWaitEvent(ml->side, ml->ev_fork, 0));
+  MXM_CUDA(launch_plan(l->ex_dev, l->V, l->E, T, l->d, v_off, (int)w.g_max, w.task_cap, (Task*)P(w.tasks),
+                       (int32_t*)P(w.meta), (int32_t*)P(w.grp_n1), (int32_t*)P(w.grp_nq), (int32_t*)P(w.p1_done),
+                       (int32_t*)P(w.hq_done), ml->side));
+  MXM_CUDA(cudaEventRecord(ml->ev_join, ml->side));
   // S2 activation quantize + gather
   MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
                                (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), (uint32_t*)P(w.hmax), st));
   mark(2);
-  // S3 plan
-  MXM_CUDA(launch_plan(l->ex_dev, l->V, l->E, T, l->d, v_off, (int)w.g_max, w.task_cap, (Task*)P(w.tasks),
-                       (int32_t*)P(w.meta), (int32_t*)P(w.grp_n1), (int32_t*)P(w.grp_nq), (int32_t*)P(w.p1_done),
-                       (int32_t*)P(w.hq_done), st));
-  mark(3);
+  MXM_CUDA(cudaStreamWaitEvent(st, ml->ev_join, 0));
+  mark(3);  // the plan's time beyond the gather's (usually ~0)
   // S4-S7 persistent group GEMM
   GemmParams prm;
   memset(&prm, 0, sizeof(prm));
