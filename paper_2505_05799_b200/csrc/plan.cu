@@ -15,6 +15,9 @@
 namespace mxm {
 
 constexpr int kPlanThreads = 1024;
+#ifndef MXM_NMAJOR_MIN_GROUPS
+#define MXM_NMAJOR_MIN_GROUPS 8  // experts with at least this many full m-tiles are emitted n-tile-major (0 = off)
+#endif
 constexpr int kMaxV = 256;
 
 // exclusive block-wide scan of one int per thread (kPlanThreads threads); returns the block total
@@ -194,26 +197,36 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
   int64_t o1 = e1, oq = (int64_t)t1 + eq, o2 = (int64_t)t1 + tq + e2;
   for (int g = g0; g < g1; ++g) {
     Task t;
-    t.expert = (uint16_t)grp_v[g];
+    const int v = grp_v[g];
+    t.expert = (uint16_t)v;
     t.row0 = grp_row0[g];
     t.rows = (uint16_t)grp_rows[g];
     t.nt = (uint8_t)grp_nt[g];
     t.gid = g;
+    // an expert with many full m-tiles (e.g. a shared expert over all T tokens) is emitted n-tile-major
+    // within its (contiguous) block of full groups: CTAs running side by side then share one weight tile
+    // in L2 and stream different token tiles, instead of sharing a token tile and each streaming its own
+    // weight tile (a large expert's weights do not fit in L2 and were re-read from HBM per m-tile)
+    const int nf = s_nfull[v], i = g - s_base[v];
+    const bool nmajor = MXM_NMAJOR_MIN_GROUPS > 0 && nf >= MXM_NMAJOR_MIN_GROUPS && i >= 0 && i < nf;
+    const int n1 = grp_n1[g], n2 = grp_n2[g];
     t.phase = 0;
-    for (int j = 0; j < grp_n1[g]; ++j) {
+    for (int j = 0; j < n1; ++j) {
       t.ntile = (uint16_t)j;
-      tasks[o1++] = t;
+      tasks[nmajor ? o1 - (int64_t)i * n1 + (int64_t)j * nf + i : o1 + j] = t;
     }
+    o1 += n1;
     t.phase = 1;
     for (int j = 0; j < grp_nq[g]; ++j) {
       t.ntile = (uint16_t)j;  // 32-row sub-chunk index
       tasks[oq++] = t;
     }
     t.phase = 2;
-    for (int j = 0; j < grp_n2[g]; ++j) {
+    for (int j = 0; j < n2; ++j) {
       t.ntile = (uint16_t)j;  // down tile (or tile pair) index
-      tasks[o2++] = t;
+      tasks[nmajor ? o2 - (int64_t)i * n2 + (int64_t)j * nf + i : o2 + j] = t;
     }
+    o2 += n2;
   }
   __syncthreads();  // every thread has read its grp_n2 entries before the scratch is cleared
   for (int g = tid; g < G; g += kPlanThreads) hq_done[g] = 0;
