@@ -104,7 +104,7 @@ struct WsLayout {
   int64_t R, g_max, task_cap;
   int64_t err, route_scratch, counts, v_off, row_src, row_w, row_exp, inv;
   int64_t Xb, XqA, XsA, XqB, XsB, H, Hq, Hs, hmax, O;
-  int64_t tasks, meta, grp_n1, grp_nq, p1_done, hq_done;
+  int64_t tasks, meta, grp_n1, grp_nq, p1_done, hq_done, P, red_cnt;
   int64_t total;
 };
 
@@ -144,6 +144,9 @@ static WsLayout make_layout(const mxm_layer* l, int64_t T, int k) {
   w.grp_nq = take(4 * w.g_max);
   w.p1_done = take(4 * w.g_max);
   w.hq_done = take(4 * w.g_max);
+  const bool split = R <= kSplitRows;  // split-K only at tiny T (bounded partial buffer)
+  w.P = split ? take((int64_t)4 * kSplitMax * kSplitRows * l->d) : -1;
+  w.red_cnt = split ? take(4 * w.g_max * (l->d / 128)) : -1;
   w.total = o;
   return w;
 }
@@ -377,7 +380,7 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   MXM_CUDA(cudaStreamWaitEvent(ml->side, ml->ev_fork, 0));
   MXM_CUDA(launch_plan(l->ex_dev, l->V, l->E, T, l->d, v_off, (int)w.g_max, w.task_cap, (Task*)P(w.tasks),
                        (int32_t*)P(w.meta), (int32_t*)P(w.grp_n1), (int32_t*)P(w.grp_nq), (int32_t*)P(w.p1_done),
-                       (int32_t*)P(w.hq_done), ml->side));
+                       (int32_t*)P(w.hq_done), (int32_t*)P(w.red_cnt), ml->side));
   MXM_CUDA(cudaEventRecord(ml->ev_join, ml->side));
   // S2 activation quantize + gather
   MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
@@ -415,6 +418,8 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   prm.hmax = (uint32_t*)P(w.hmax);
   prm.O = (uint16_t*)P(w.O);
   prm.row_w = row_w;
+  prm.P = (float*)P(w.P);
+  prm.red_cnt = (int32_t*)P(w.red_cnt);
   prm.d = l->d;
   prm.f_max = l->f_max;
   prm.prof = reinterpret_cast<unsigned long long*>(l->prof_counters);

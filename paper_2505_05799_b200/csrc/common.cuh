@@ -77,6 +77,25 @@ struct Task {
 };
 static_assert(sizeof(Task) == 16, "task size");
 
+// Split-K of phase-2 (down) tasks: when a launch has fewer down tasks than SMs (tiny T, e.g.
+// Mixtral T <= 256) each down task of a streaming-epilogue expert is cut into S <= kSplitMax K-slices (meta[7]);
+// slices write fp32 partials, the last-arriving slice reduces them in fixed slice order (deterministic).
+// A phase-2 task's ntile holds the tile (pair) index in bits 0-9 and the slice in bits 10-13.
+constexpr int kSplitMax = 4;
+constexpr int kSplitRows = 512;  // split only when the launch has <= this many route rows (partial buffer size)
+__host__ __device__ inline int task_tile(const Task& t) { return t.phase == 2 ? (t.ntile & 0x3FF) : t.ntile; }
+__host__ __device__ inline int task_slice(const Task& t) { return t.phase == 2 ? (t.ntile >> 10) : 0; }
+__host__ __device__ inline bool down_splittable(const ExpertDesc& e) {
+  return !(kind_is_i8(e.blk[2].geo.kind) && e.blk[2].geo.group == 128);  // g128 W-A downs drain per group
+}
+// stage range [ks0, ks1) of slice `sl` of S over ns stages (slices of an even number of stages so a g128 / g64
+// weight-only group never straddles two slices)
+__host__ __device__ inline void split_range(int ns, int S, int sl, int& ks0, int& ks1) {
+  const int per = (((ns + S - 1) / S) + 1) & ~1;
+  ks0 = sl * per;
+  ks1 = ks0 + per < ns ? ks0 + per : ns;
+}
+
 // Token-tile cap of an expert's m-tiles: dual gate/up tiles of up to MXM_DUAL_TILE tokens fit one TMEM
 // accumulator buffer (2 x 160 columns next to a 3-slot A ring); register-accumulated tiles (g128 W-A dual, or gate and up as two sub-loops) keep
 // 64 columns per warpgroup half in registers -> 64 tokens.

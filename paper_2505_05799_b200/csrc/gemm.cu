@@ -67,6 +67,7 @@ struct Ctl {
   uint64_t tfull[kRing], tempty[kRing];
   Task ring[kRing];
   uint32_t tmem_base;
+  int red_last;  // split-K: this CTA's slice arrived last (epilogue broadcast)
   uint32_t colmax[2][2][4][8];  // [buffer][warpgroup][lane quarter][column] for the fused g128 h-quant
   alignas(16) float cw[8][2][64];  // per epilogue warp: [0] activation scale of the current drain event,
                                    // [1] route weight of this warp's token columns (broadcast reads)
@@ -77,6 +78,7 @@ struct SubLoop {
   const LinDesc* mat[2];
   int tile[2];                           // 128-channel output tile of each mat
   int nmats, bmap, ns, i8, xform, g128;  // xform: bit m set = mat m needs the packed->A transform
+  int ks0, ks1;                           // stage range (a split-K slice of a down task, else [0, ns))
 };
 
 __device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, int bmap, int tile0, int tile1) {
@@ -91,13 +93,17 @@ __device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, i
   s.i8 = kind_is_i8(a->geo.kind);
   s.xform = (kind_needs_transform(a->geo.kind) ? 1 : 0) | ((b && kind_needs_transform(b->geo.kind)) ? 2 : 0);
   s.g128 = s.i8 && a->geo.group == 128;
+  s.ks0 = 0;
+  s.ks1 = s.ns;
   return s;
 }
 
 // phase 0: gate & up share the token tile (one sub-loop when dual); phase 2: a task covers down tiles
 // (2j, 2j+1) as two mats sharing the h tile when down_pair() (common.cuh), else tile j alone
-__device__ __forceinline__ int build_subloops(const Task& t, const ExpertDesc* __restrict__ ex, int d, SubLoop* sl) {
+__device__ __forceinline__ int build_subloops(const Task& t, const ExpertDesc* __restrict__ ex, int d, int S,
+                                              SubLoop* sl) {
   const ExpertDesc& e = ex[t.expert];
+  const int tile = task_tile(t);
   if (t.phase == 0) {
     if (e.dual) {
       sl[0] = make_sl(&e.blk[0], &e.blk[1], e.blk[0].in_slot, t.ntile, t.ntile);
@@ -109,12 +115,13 @@ __device__ __forceinline__ int build_subloops(const Task& t, const ExpertDesc* _
   }
   const int nd = d / 128;
   if (down_pair(e, t.nt, nd)) {
-    const int j0 = 2 * t.ntile;
+    const int j0 = 2 * tile;
     const bool two = j0 + 1 < nd;
     sl[0] = make_sl(&e.blk[2], two ? &e.blk[2] : nullptr, 3 + e.blk[2].in_slot, j0, j0 + 1);
   } else {
-    sl[0] = make_sl(&e.blk[2], nullptr, 3 + e.blk[2].in_slot, t.ntile, t.ntile);
+    sl[0] = make_sl(&e.blk[2], nullptr, 3 + e.blk[2].in_slot, tile, tile);
   }
+  if (S > 1 && down_splittable(e)) split_range(sl[0].ns, S, task_slice(t), sl[0].ks0, sl[0].ks1);
   return 1;
 }
 
@@ -676,6 +683,9 @@ __device__ __forceinline__ void mma_subloop_mode(Ctl& ctl, uint8_t* smem, uint32
 }
 
 // ---------------------------------------------------------------- the kernel
+// SPLIT: the launch may cut downs into K-slices (tiny T, workspace has the partial buffer). A separate
+// instantiation, so the split-K bookkeeping costs the large-T kernel no registers.
+template <bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   // keep the pointer in the shared window (no uintptr_t round trip) so tile accesses compile to LDS/STS
@@ -724,6 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = ctl.tmem_base;
   const int n_tasks = p.meta[0];
+#define n_split (SPLIT ? p.meta[7] : 1)  // split-K slices of splittable downs (plan; common.cuh)
   // wait-site cycle counters: compiled in only for the diagnostic build (tools/diag_waits.py); in the
   // product build they fold away (they would otherwise pin 32 registers in every role)
 #ifdef MXM_DEBUG_COUNTERS
@@ -781,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           fence_proxy_async_global();
         }
         SubLoop sl[2];
-        const int nsl = build_subloops(t, p.ex, p.d, sl);
+        const int nsl = build_subloops(t, p.ex, p.d, n_split, sl);
         const int nti = nt_index(t.nt);
         for (int si = 0; si < nsl; ++si) {
           const SubLoop s = sl[si];
@@ -792,27 +803,41 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const uint32_t cb0 = (uint32_t)g0.code_bytes, mb0 = (uint32_t)g0.meta_bytes;
           const uint32_t cb1 = (uint32_t)g1.code_bytes, mb1 = (uint32_t)g1.meta_bytes;
           const int gst0 = g0.group / g0.ks, gst1 = g1.group / g1.ks;
-          const uint8_t* src0 = s.mat[0]->packed + (int64_t)s.tile[0] * g0.rb_bytes;
-          const uint8_t* src1 = s.nmats == 2 ? s.mat[1]->packed + (int64_t)s.tile[1] * g1.rb_bytes : nullptr;
+          const int ksb = SPLIT ? s.ks0 : 0, kse = SPLIT ? s.ks1 : s.ns;
+          const uint8_t* src0 = s.mat[0]->packed + (SPLIT ? chunk_offset(g0, s.tile[0], ksb) : (int64_t)s.tile[0] * g0.rb_bytes);
+          const uint8_t* src1 = s.nmats == 2 ? s.mat[1]->packed + (SPLIT ? chunk_offset(g1, s.tile[1], ksb)
+                                                                            : (int64_t)s.tile[1] * g1.rb_bytes)
+                                             : nullptr;
           uint8_t* const dst0 = tileX(0, 0);
           uint8_t* const dst1 = tileX(0, 1);
           const int str0 = kSlotBytes, str1 = kSlotBytes;
           const int kstep = s.i8 ? 128 : 64;
-          int gc0 = 0, gc1 = 0;
-          for (int ks = 0; ks < s.ns; ++ks) {
+          int gc0 = SPLIT ? ksb % gst0 : 0, gc1 = SPLIT ? ksb % gst1 : 0;
+          // a split-K slice that starts inside a weight-only group: its first stage is laid out as a group
+          // start, [group meta (copied from the group-start chunk) | codes], so the transform needs no case
+          const uint8_t* gm0 = (SPLIT && gc0 != 0 && g0.kind == KIND_WO)
+                                   ? s.mat[0]->packed + chunk_offset(g0, s.tile[0], ksb - gc0) : nullptr;
+          const uint8_t* gm1 = (SPLIT && src1 && gc1 != 0 && g1.kind == KIND_WO)
+                                   ? s.mat[1]->packed + chunk_offset(g1, s.tile[1], ksb - gc1) : nullptr;
+          for (int ks = ksb; ks < kse; ++ks) {
             const uint32_t c0 = cb0 + (gc0 == 0 ? mb0 : 0u);
             const uint32_t c1 = src1 ? cb1 + (gc1 == 0 ? mb1 : 0u) : 0u;
+            const uint32_t e0 = SPLIT && gm0 ? mb0 : 0u, e1 = SPLIT && gm1 ? mb1 : 0u;
             if (++gc0 == gst0) gc0 = 0;
             if (++gc1 == gst1) gc1 = 0;
             twait(&ctl.empty[stage], sphase ^ 1, pc[1], prof_on);
             TR(0, n_tr_p);
             ++n_tr_p;
-            mbar_arrive_expect_tx(&ctl.full[stage], (uint32_t)t.nt * 128u + c0 + c1);
-            bulk_load(dst0 + stage * str0, src0, c0, &ctl.full[stage]);
+            mbar_arrive_expect_tx(&ctl.full[stage], (uint32_t)t.nt * 128u + c0 + c1 + e0 + e1);
+            if (e0) bulk_load(dst0 + stage * str0, gm0, e0, &ctl.full[stage]);
+            bulk_load(dst0 + stage * str0 + e0, src0, c0, &ctl.full[stage]);
             src0 += c0;
+            gm0 = nullptr;
             if (src1) {
-              bulk_load(dst1 + stage * str1, src1, c1, &ctl.full[stage]);
+              if (e1) bulk_load(dst1 + stage * str1, gm1, e1, &ctl.full[stage]);
+              bulk_load(dst1 + stage * str1 + e1, src1, c1, &ctl.full[stage]);
               src1 += c1;
+              gm1 = nullptr;
             }
             tma_load_2d(tileB(stage), map, &ctl.full[stage], ks * kstep, t.row0);
             if (s.g128) {  // the 128-K group's scales into the scale ring (read by the epilogue)
@@ -860,11 +885,12 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       if (phase == 255) break;
       if (phase == 1) continue;
       SubLoop sl[2];
-      const int nsl = (int)bcast((uint32_t)build_subloops(t, p.ex, p.d, sl));
+      const int nsl = (int)bcast((uint32_t)build_subloops(t, p.ex, p.d, n_split, sl));
       const uint32_t nt = bcast(t.nt);
       for (int si = 0; si < nsl; ++si) {
         const SubLoop s = sl[si];
-        const uint32_t ns = bcast((uint32_t)s.ns), g128 = bcast((uint32_t)s.g128), xf = bcast((uint32_t)s.xform);
+        const uint32_t ns = bcast((uint32_t)(SPLIT ? s.ks1 - s.ks0 : s.ns)), g128 = bcast((uint32_t)s.g128);
+        const uint32_t xf = bcast((uint32_t)s.xform);
         const uint32_t i8 = bcast((uint32_t)s.i8), two = bcast((uint32_t)(s.nmats == 2));
         MmaState st{stage, sphase, abuf, acc_ph, aidx, ntr_m};
 #if defined(MXM_PROF_SUBLOOP) && defined(MXM_DEBUG_COUNTERS)
@@ -911,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       if (t.phase == 255) break;
       if (t.phase == 1) continue;
       SubLoop sl[2];
-      const int nsl = build_subloops(t, p.ex, p.d, sl);
+      const int nsl = build_subloops(t, p.ex, p.d, n_split, sl);
       for (int si = 0; si < nsl; ++si) {
         const SubLoop s = sl[si];
         const bool two = s.nmats == 2;
@@ -925,8 +951,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         const uint32_t offB = (0x4300u | (symB ? (1u << (bitsB - 1)) : 0u)) * 0x10001u;
         const bool xa = (s.xform & 1) != 0, xb = two && (s.xform & 2) != 0;
         uint32_t sa = 0, za = 0, sb = 0, zb = 0;
-        int gca = 0, gcb = 0;
-        for (int ks = 0; ks < s.ns; ++ks) {
+        int gca = 0, gcb = 0;  // a split-K slice's first stage is laid out as a group start (producer)
+        for (int ks = SPLIT ? s.ks0 : 0; ks < (SPLIT ? s.ks1 : s.ns); ++ks) {
           const bool hmA = gca == 0, hmB = gcb == 0;
           if (++gca == gstA) gca = 0;
           if (++gcb == gstB) gcb = 0;
@@ -1049,7 +1075,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         continue;
       }
       SubLoop sl[2];
-      const int nsl = build_subloops(t, p.ex, p.d, sl);
+      const int nsl = build_subloops(t, p.ex, p.d, n_split, sl);
       const bool reg_mode = nsl == 2 || sl[0].g128;
       const int half = t.nt >> 1;
       const int col0 = wg * half;
@@ -1073,6 +1099,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       if (!reg_mode) {
         // ======== streaming epilogue: one drain event for the whole task (dual phase 0, or phase 2)
         const SubLoop s = sl[0];
+        const bool split = SPLIT && s.ks1 - s.ks0 != s.ns;
+        const int slice = task_slice(t);
         const bool two = s.nmats == 2;
         const float* xs_s = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;  // group-major [g][R]
         float sw0 = 1.f, sw1 = 1.f, sa_lo = 1.f, sa_hi = 1.f;
@@ -1150,6 +1178,16 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 #pragma unroll
             for (int j = 0; j < 8; ++j) hb[j] = f2bf(silu_f(fa[j]) * fb[j]);
             emit_h8(p, t, dmode, dqmax, n, col0 + c, nvalid - c, hb, ctl, wg, q, lane, rbuf);
+          } else if (split) {  // split-K slice: fp32 partial sums (reduced below by the last slice)
+            float* q0 = p.P + ((int64_t)slice * kSplitRows + t.row0 + col0 + c) * p.d + n;
+            float* q1 = p.P + ((int64_t)slice * kSplitRows + t.row0 + col0 + c) * p.d + n1;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (c + j < nvalid) {
+                __stcg(q0 + (int64_t)j * p.d, fa[j]);
+                if constexpr (TWO) __stcg(q1 + (int64_t)j * p.d, fb[j]);
+              }
+            }
           } else {
             const float4 r0 = *reinterpret_cast<const float4*>(cw_rw + c);
             const float4 r1 = *reinterpret_cast<const float4*>(cw_rw + c + 4);
@@ -1181,6 +1219,33 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         if (lane == 0) mbar_arrive(&ctl.acce[b0]);
         if (threadIdx.x == 256) TR(6, n_tr_e);
         ++n_tr_e;
+        if (split) {
+          // the last-arriving slice of this (m-tile, down tile) sums the slices' partials in slice order
+          named_bar_sync(1, 256);
+          if (ew == 0 && lane == 0) {
+            __threadfence();
+            const int old = atomicAdd(p.red_cnt + (int64_t)t.gid * (p.d / 128) + task_tile(t), 1);
+            ctl.red_last = old == n_split - 1;
+            __threadfence();
+          }
+          named_bar_sync(1, 256);
+          if (ctl.red_last) {
+            const bool two = s.nmats == 2;
+            for (int c = 0; c < half; ++c) {
+              if (c >= nvalid) break;
+              const int64_t row = (int64_t)t.row0 + col0 + c;
+              float a0 = 0.f, a1 = 0.f;
+              for (int q2 = 0; q2 < n_split; ++q2) {
+                const float* pr = p.P + ((int64_t)q2 * kSplitRows + row) * p.d;
+                a0 += __ldcg(pr + n);
+                if (two) a1 += __ldcg(pr + n1);
+              }
+              const float rw = cw_rw[c];
+              p.O[row * p.d + n] = f2bf(a0 * rw);
+              if (two) p.O[row * p.d + n1] = f2bf(a1 * rw);
+            }
+          }
+        }
       } else {
         // ======== register-accumulating epilogue (g128 drains / hetero gate-up sub-loops)
         float2 acc2[32];
@@ -1339,11 +1404,16 @@ cudaError_t debug_nan_info(unsigned long long* out, bool reset) {
 cudaError_t launch_moe_gemm(const GemmParams& prm, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(moe_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(moe_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(moe_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  moe_gemm_kernel<<<grid, kThreads, kSmemBytes, st>>>(prm);
+  if (prm.P != nullptr)
+    moe_gemm_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(prm);
+  else
+    moe_gemm_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(prm);
   return cudaGetLastError();
 }
 

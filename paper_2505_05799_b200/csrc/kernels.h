@@ -25,6 +25,8 @@ struct GemmParams {
   uint32_t* hmax;  // per route row: max |h| (fp32 bits) for per-token W-A downs (order-independent atomicMax)
   uint16_t* O;
   const float* row_w;
+  float* P;          // split-K fp32 partials [kSplitMax][kSplitRows][d] (nullptr: no split-K this launch)
+  int32_t* red_cnt;  // split-K arrival counters [group][d/128]
   int d, f_max;
   unsigned long long* prof;  // optional [grid][16] cycle counters per wait site (nullptr = off)
 };
@@ -49,7 +51,7 @@ cudaError_t launch_combine(const void* O, int d, int64_t T, int k, int S, const 
                            cudaStream_t st);
 cudaError_t launch_plan(const ExpertDesc* ex, int V, int E, int64_t T, int d, const int32_t* v_off, int g_max,
                         int64_t task_cap, Task* tasks, int32_t* meta, int32_t* grp_n1, int32_t* grp_nq,
-                        int32_t* p1_done, int32_t* hq_done, cudaStream_t st);
+                        int32_t* p1_done, int32_t* hq_done, int32_t* red_cnt, cudaStream_t st);
 cudaError_t launch_moe_gemm(const GemmParams& prm, int grid, cudaStream_t st);
 cudaError_t launch_ep_route(const int32_t* ids, int64_t T, int k, int E, int G, int32_t* dest_counts, int32_t* pos,
                             int32_t* err, cudaStream_t st);

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
                                                             int64_t task_cap, Task* __restrict__ tasks,
                                                             int32_t* __restrict__ meta, int32_t* __restrict__ grp_n1,
                                                             int32_t* __restrict__ grp_nq, int32_t* __restrict__ p1_done,
-                                                            int32_t* __restrict__ hq_done) {
+                                                            int32_t* __restrict__ hq_done, int32_t* __restrict__ red_cnt) {
   __shared__ int s_cap[kMaxV], s_nfull[kMaxV], s_rem[kMaxV], s_base[kMaxV], s_ragid[kMaxV];
   __shared__ float s_cf[kMaxV], s_cr[kMaxV];
   __shared__ int s_order[kMaxV];
@@ -182,7 +182,32 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
   int t1, tq, t2;
   const int e1 = block_excl_scan(c1, s_wt, &t1);
   const int eq = block_excl_scan(cq, s_wt, &tq);
-  const int e2 = block_excl_scan(c2, s_wt, &t2);
+  int e2 = block_excl_scan(c2, s_wt, &t2);
+  // split-K of the downs when they cannot fill the SMs (common.cuh); red_cnt == nullptr: not allowed
+  __shared__ int s_minns;
+  if (tid == 0) s_minns = 1 << 30;
+  __syncthreads();
+  if (tid < V && down_splittable(ex[tid])) atomicMin(&s_minns, ex[tid].blk[2].geo.ns);
+  __syncthreads();
+  int S = 1;
+  if (red_cnt != nullptr && t2 > 0 && t2 < kNumSms && s_minns < (1 << 30)) {
+    S = min(kSplitMax, (kNumSms + t2 - 1) / t2);
+    for (; S > 1; --S) {
+      int a, b;
+      split_range(s_minns, S, S - 1, a, b);
+      if (b - a >= 2) break;
+    }
+  }
+  if (S > 1) {
+    const int nd = d / 128;
+    c2 = 0;
+    for (int g = g0; g < g1; ++g) {
+      if (down_splittable(ex[grp_v[g]])) grp_n2[g] *= S;
+      c2 += grp_n2[g];
+    }
+    e2 = block_excl_scan(c2, s_wt, &t2);
+    for (int i = tid; i < G * nd; i += kPlanThreads) red_cnt[i] = 0;
+  }
   const int64_t total = (int64_t)t1 + tq + t2;
   if (tid == 0) {
     meta[0] = total <= task_cap ? (int32_t)total : -1;
@@ -192,6 +217,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
     meta[4] = G;
     meta[5] = 0;  // queue head
     meta[6] = 0;  // executed-task counter (debug)
+    meta[7] = S;  // split-K slices of splittable down tasks
   }
   if (total > task_cap) return;
   int64_t o1 = e1, oq = (int64_t)t1 + eq, o2 = (int64_t)t1 + tq + e2;
@@ -222,8 +248,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
       tasks[oq++] = t;
     }
     t.phase = 2;
+    const int S_g = (S > 1 && down_splittable(ex[v])) ? S : 1;
     for (int j = 0; j < n2; ++j) {
-      t.ntile = (uint16_t)j;  // down tile (or tile pair) index
+      t.ntile = (uint16_t)((j / S_g) | ((j % S_g) << 10));  // down tile (or pair) index | K-slice << 10
       tasks[nmajor ? o2 - (int64_t)i * n2 + (int64_t)j * nf + i : o2 + j] = t;
     }
     o2 += n2;
@@ -234,10 +261,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
 
 cudaError_t launch_plan(const ExpertDesc* ex, int V, int E, int64_t T, int d, const int32_t* v_off, int g_max,
                         int64_t task_cap, Task* tasks, int32_t* meta, int32_t* grp_n1, int32_t* grp_nq,
-                        int32_t* p1_done, int32_t* hq_done, cudaStream_t st) {
+                        int32_t* p1_done, int32_t* hq_done, int32_t* red_cnt, cudaStream_t st) {
   if (V > kMaxV) return cudaErrorInvalidValue;
   plan_kernel<<<1, kPlanThreads, 0, st>>>(ex, V, E, T, d, v_off, g_max, task_cap, tasks, meta, grp_n1, grp_nq, p1_done,
-                                          hq_done);
+                                          hq_done, red_cnt);
   return cudaGetLastError();
 }
 

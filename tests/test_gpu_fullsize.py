@@ -79,12 +79,15 @@ def test_mixtral_crossover_mix(mx, T):
     assert e <= TOL, e
 
 
-def test_mixtral_single_token(mx):
-    """Mixtral at T=1: two experts, memory-bound, split across the whole grid."""
+@pytest.mark.parametrize("T", [1, 16])
+def test_mixtral_small_t(mx, T):
+    """Mixtral at T=1 / 16: memory-bound, the downs split-K across the grid."""
     cfg = C.get_config("mx")
-    table = C.precision_table(cfg, 1)
-    ids, _ = gen_routing(1, cfg.n_routed, cfg.top_k, seed=0)
-    case, ol, rows = _sampled_case(cfg, table, 1, ids[0].tolist())
+    table = C.precision_table(cfg, T)
+    ids, _ = gen_routing(T, cfg.n_routed, cfg.top_k, seed=0)
+    cnt = np.bincount(ids.ravel(), minlength=cfg.n_routed)
+    P = ids[0].tolist() if T == 1 else np.argsort(-cnt)[:3].tolist()
+    case, ol, rows = _sampled_case(cfg, table, T, P)
     e = _check(case, ol, rows)
     assert e <= TOL, e
 

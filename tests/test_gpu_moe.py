@@ -117,3 +117,17 @@ def test_wide_tile_single_mat_g128_down(mx):
     case = make_case(TINY, table, 300, seed=9)
     e, _, _ = _parity(case)
     assert e <= TOL, e
+
+
+def test_split_k_downs(mx):
+    """Few down tasks (T=8): the downs are cut into K-slices whose fp32 partials the last slice reduces in
+    fixed order. Covers a per-channel weight-only down (slices start mid-group: meta copy),
+    g128 weight-only, per-channel W-A, and an unsplittable g128 W-A down in the same launch; deterministic."""
+    cfg = C.LayerConfig("splitk", 4, 0, 512, 1024, 0, 2, 8)
+    table = [[C.WO(4, 128), C.WO(4, 128), C.WO(2, -1)], [C.WO(4, 128), C.WO(4, 128), C.WO(3, 128)],
+             [C.WA(8, -1), C.WA(8, -1), C.WA(8, -1)], [C.WA(4, 128), C.WA(4, 128), C.WA(4, 128)]]
+    for T in (1, 8):
+        case = make_case(cfg, table, T, seed=T)
+        e, layer, y = _parity(case)
+        assert e <= TOL, (T, e)
+        assert np.array_equal(gpu_run(layer, case), y)
