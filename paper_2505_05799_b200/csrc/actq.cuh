@@ -63,4 +63,66 @@ __device__ __forceinline__ float quant_group_warp(const uint16_t* src, int8_t* _
   return s;
 }
 
+// One whole row of d bf16 values (d % 128 == 0, d <= 128 * MAXG) quantized by one warp in groups of g
+// (128, or g == d for per-token scales): the row is loaded once into registers (lane l holds elements
+// 128*i + 4l .. +3 of chunk i), all loads in flight together; same arithmetic as quant_group_warp.
+// Scales go to sc[gi * R] (group-major [g][R]).
+template <int MAXG>
+__device__ __forceinline__ void quant_row_warp(const uint16_t* __restrict__ src, int8_t* __restrict__ dst, int d, int g,
+                                               int qmax, float* __restrict__ sc, int64_t R) {
+  const int lane = threadIdx.x & 31;
+  const int nch = d / 128;
+  uint2 v[MAXG];
+#pragma unroll
+  for (int i = 0; i < MAXG; ++i)
+    if (i < nch) v[i] = *reinterpret_cast<const uint2*>(src + 128 * i + 4 * lane);
+  auto absmax4 = [](uint2 x) {
+    return fmaxf(fmaxf(fabsf(bf16_bits_to_float(x.x & 0xFFFFu)), fabsf(bf16_bits_to_float(x.x >> 16))),
+                 fmaxf(fabsf(bf16_bits_to_float(x.y & 0xFFFFu)), fabsf(bf16_bits_to_float(x.y >> 16))));
+  };
+  const float fq = (float)qmax;
+  auto quant4 = [&](uint2 x, float r) {
+    const float f[4] = {bf16_bits_to_float(x.x & 0xFFFFu), bf16_bits_to_float(x.x >> 16),
+                        bf16_bits_to_float(x.y & 0xFFFFu), bf16_bits_to_float(x.y >> 16)};
+    uint32_t packed = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float q = rintf(__fmul_rn(f[j], r));
+      q = fminf(fmaxf(q, -fq), fq);
+      packed |= (uint32_t)((int)q & 0xFF) << (8 * j);
+    }
+    return packed;
+  };
+  if (g == 128) {  // one group per 128-element chunk
+#pragma unroll
+    for (int i = 0; i < MAXG; ++i) {
+      if (i < nch) {
+        const float amax = warp_max(absmax4(v[i]));
+        float r = 0.f, s = 1.f;
+        if (amax > 0.f) {
+          r = __fdiv_rn(fq, amax);
+          s = __fdiv_rn(amax, fq);
+        }
+        *reinterpret_cast<uint32_t*>(dst + 128 * i + 4 * lane) = quant4(v[i], r);
+        if (lane == 0) sc[(int64_t)i * R] = s;
+      }
+    }
+  } else {  // per token: one group = the row
+    float amax = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXG; ++i)
+      if (i < nch) amax = fmaxf(amax, absmax4(v[i]));
+    amax = warp_max(amax);
+    float r = 0.f, s = 1.f;
+    if (amax > 0.f) {
+      r = __fdiv_rn(fq, amax);
+      s = __fdiv_rn(amax, fq);
+    }
+#pragma unroll
+    for (int i = 0; i < MAXG; ++i)
+      if (i < nch) *reinterpret_cast<uint32_t*>(dst + 128 * i + 4 * lane) = quant4(v[i], r);
+    if (lane == 0) sc[0] = s;
+  }
+}
+
 }  // namespace mxm

@@ -16,7 +16,7 @@ namespace mxm {
 
 constexpr int kPlanThreads = 1024;
 #ifndef MXM_NMAJOR_MIN_GROUPS
-#define MXM_NMAJOR_MIN_GROUPS 8  // experts with at least this many full m-tiles are emitted n-tile-major (0 = off)
+#define MXM_NMAJOR_MIN_GROUPS 2  // experts with at least this many full m-tiles are emitted n-tile-major (0 = off)
 #endif
 constexpr int kMaxV = 256;
 

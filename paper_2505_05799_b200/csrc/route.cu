@@ -160,6 +160,9 @@ __global__ void route_shared_kernel(int64_t T, int E, int S, const float* __rest
 }
 
 // ---- S2: one warp per route row: gather / quantize the gate/up inputs of the row's expert
+// QUANT: the layer has weight-activation input slots (the row-in-registers quantizer needs ~124 registers;
+// an all-weight-only layer launches the copy-only instantiation at full occupancy)
+template <bool QUANT>
 __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const int32_t* __restrict__ row_src,
                                     const int32_t* __restrict__ row_exp, const int32_t* __restrict__ v_off, int V,
                                     const ExpertDesc* __restrict__ ex,
@@ -177,17 +180,22 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
     const LinDesc& L = E.blk[b];
     if (b == 1 && E.blk[1].in_slot == E.blk[0].in_slot) break;
     if (L.in_slot == 0) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(src);
-      uint4* d4 = reinterpret_cast<uint4*>(Xb + row * d);
+      const uint4* __restrict__ s4 = reinterpret_cast<const uint4*>(src);
+      uint4* __restrict__ d4 = reinterpret_cast<uint4*>(Xb + row * d);
+#pragma unroll 4
       for (int i = lane; i < d / 8; i += 32) d4[i] = s4[i];
-    } else {
+    } else if constexpr (QUANT) {
       int8_t* q = (L.in_slot == 1 ? XqA : XqB) + row * d;
       float* sc = (L.in_slot == 1 ? XsA : XsB) + row;  // group-major [g][R]
       const int g = L.a_group == -1 ? d : L.a_group;
       const int qmax = (1 << (L.a_bits - 1)) - 1;
-      for (int gi = 0; gi < d / g; ++gi) {
-        const float s = quant_group_warp(src + gi * g, q + gi * g, g, qmax, nullptr);
-        if (lane == 0) sc[gi * R] = s;
+      if (d <= 128 * 32 && (g == 128 || g == d)) {
+        quant_row_warp<32>(src, q, d, g, qmax, sc, R);  // whole row in registers, all loads in flight
+      } else {
+        for (int gi = 0; gi < d / g; ++gi) {
+          const float s = quant_group_warp(src + gi * g, q + gi * g, g, qmax, nullptr);
+          if (lane == 0) sc[gi * R] = s;
+        }
       }
     }
   }
@@ -268,8 +276,14 @@ cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, co
                                 const ExpertDesc* ex, int64_t R, void* Xb, void* XqA, float* XsA, void* XqB, float* XsB,
                                 uint32_t* hmax, cudaStream_t st) {
   if (R <= 0) return cudaSuccess;
-  gather_quant_kernel<<<(unsigned)((R * 32 + 255) / 256), 256, 0, st>>>(
-      (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB, hmax);
+  if (XqA != nullptr || XqB != nullptr)
+    gather_quant_kernel<true><<<(unsigned)((R * 32 + 255) / 256), 256, 0, st>>>(
+        (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB,
+        hmax);
+  else
+    gather_quant_kernel<false><<<(unsigned)((R * 32 + 255) / 256), 256, 0, st>>>(
+        (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB,
+        hmax);
   return cudaGetLastError();
 }
 
