@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 from synth import configs as C  # noqa: E402
 from synth.gen import gen_activations, gen_routing, gen_shared_weights, gen_weight, weight_seed  # noqa: E402
 
-METRIC = "MoE-block tokens/s (% of per-expert roofline) vs bf16 & uniform"
+METRIC = "MoE-block tokens/s at 1/2/4/8 B200 and % of per-expert roofline vs bf16 & uniform"  # BASELINE.json
 L2_FLUSH_BYTES = 256 << 20
 
 
