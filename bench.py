@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--table", default="mixed", help="mixed | w16 | <scheme name, e.g. w2a16_g128_asym>")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=256, help="tokens in the cpu_baseline oracle sample")
+    ap.add_argument("--cpu-sample", type=int, default=512, help="tokens in the cpu_baseline oracle sample")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent full replicas instead of EP")
     return ap.parse_args()
