@@ -155,6 +155,42 @@ mxm_status mxm_layer_debug_counters(mxm_layer* l, void* dev_buf);
 /* Number of library kernels one mxm_moe_group_gemm call launches (route x3-4, gather, plan, GEMM, combine). */
 int32_t mxm_kernels_per_call(const mxm_layer* l);
 
+/* ---------------------------------------------------------------- test-only introspection of the hot path
+ * Byte offsets (into the workspace of a call with T tokens, top_k routes) of the intermediate buffers the
+ * hot path writes, so that tests can compare them with the oracle after a real mxm_moe_group_gemm call.
+ * off[MXM_WS_N]; -1 = not allocated for this layer. Route rows: R = T*top_k + T*n_shared (shared experts'
+ * rows s*T + t first, then routed rows sorted by expert, stable in (t, j)).
+ *   ROW_SRC int32[R] source token   ROW_W f32[R] route weight   ROW_EXP int32[R] expert   INV int32[T*k]
+ *   XB bf16[R][hidden]          gathered bf16 gate/up input (weight-only / bf16 experts)
+ *   XQA/XQB int8[R][hidden]     activation codes of input slots A/B (two's complement for a5/a8; for a4 the
+ *                               e4m3 byte (q<0)<<7 | |q|, whose value is q * 2^-9)
+ *   XSA/XSB f32[G][R]           activation scales, group-major (G = hidden/128, or 1 per-token)
+ *   XCA/XCB int32[G][R]         per-group sum of the a4 codes (offset-binary correction of w4a4 blocks)
+ *   H bf16[R][F]  HQ int8[R][F]  HS f32[G][R]  HC int32[G][R]   the same for h (F = max inter, entry F_MAX)
+ *   O bf16[R][hidden]           per-route down output o * w_e
+ *   V_OFF int32[E+S+1] first row of each (virtual) expert;  R and F_MAX are values, not offsets. */
+enum {
+  MXM_WS_ROW_SRC = 0, MXM_WS_ROW_W, MXM_WS_ROW_EXP, MXM_WS_INV, MXM_WS_XB, MXM_WS_XQA, MXM_WS_XSA, MXM_WS_XQB,
+  MXM_WS_XSB, MXM_WS_H, MXM_WS_HQ, MXM_WS_HS, MXM_WS_O, MXM_WS_V_OFF, MXM_WS_R, MXM_WS_F_MAX, MXM_WS_XCA,
+  MXM_WS_XCB, MXM_WS_HC, MXM_WS_N
+};
+mxm_status mxm_debug_workspace_layout(const mxm_layer* l, int64_t T, int32_t top_k, int64_t* off);
+/* [sync] bytes of the accumulator dump buffer of mxm_debug_moe_group_gemm_dump for T tokens and top_k. */
+mxm_status mxm_debug_acc_bytes(const mxm_layer* l, int64_t T, int32_t top_k, int64_t* bytes);
+/* [async] mxm_moe_group_gemm (same arguments and result) through a test-only instantiation of the persistent
+ * kernel that also stores, before each drain, the raw 32-bit accumulator of every weight-activation block:
+ *   acc uint32: gate / up [2][hidden/128][R][F], then down [F/128][R][hidden] (F = max inter): element
+ *   [j][g][row][n] = accumulator of block j (0 gate, 1 up, 2 down) over K-group g (g = 0 for per-channel
+ *   blocks) for route row `row`, output channel n.
+ *   i8-kind blocks (w5a5, w8a8): the int32 sum_k q_w q_a. f8-kind blocks (w4a4): the fp32 bits of
+ *   2^-18 * sum_k (q_w + 8) q_a (exact). Entries of other blocks are left untouched.
+ * Split-K is disabled, so every accumulator covers the whole group (or the whole K). For weight-activation
+ * downs quantized in the gate/up epilogue (g128) the bf16 h is also written to the H buffer. */
+mxm_status mxm_debug_moe_group_gemm_dump(const mxm_layer* l, const void* x, int64_t T, int32_t top_k,
+                                         const int32_t* topk_ids, const float* topk_w, const float* shared_w, void* y,
+                                         void* workspace, int64_t ws_bytes, void* acc, int64_t acc_bytes,
+                                         mxm_stream stream);
+
 /* ---------------------------------------------------------------- expert parallelism
  * Rank r of G owns routed experts [r*E/G, (r+1)*E/G); tokens stay on their source rank. The host runtime
  * exchanges counts and rows with NCCL all-to-all(v) (torch.distributed on ProcessGroupNCCL); these calls

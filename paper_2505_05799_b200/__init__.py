@@ -187,19 +187,61 @@ class MoELayer:
             self._ws = torch.empty(nb, dtype=torch.uint8, device=self._desc_dev.device)
         return self._ws
 
+    def _check_args(self, x, topk_ids, topk_w, shared_w, out):
+        # every tensor is read as raw memory by the kernels: check dtype, shape, contiguity and device here
+        dev = self._desc_dev.device
+        T = x.shape[0]
+        assert x.dtype == torch.bfloat16 and x.is_contiguous() and tuple(x.shape) == (T, self.hidden), "x [T, hidden] bf16"
+        assert topk_ids.dtype == torch.int32 and topk_ids.is_contiguous() and topk_ids.dim() == 2 \
+            and topk_ids.shape[0] == T, "topk_ids [T, k] int32 contiguous"
+        k = topk_ids.shape[1]
+        assert topk_w.dtype == torch.float32 and topk_w.is_contiguous() and tuple(topk_w.shape) == (T, k), \
+            "topk_w [T, k] float32 contiguous"
+        if shared_w is not None:
+            assert shared_w.dtype == torch.float32 and shared_w.is_contiguous() and \
+                tuple(shared_w.shape) == (T, self.n_shared), "shared_w [T, n_shared] float32 contiguous"
+        if out is not None:
+            assert out.dtype == torch.bfloat16 and out.is_contiguous() and tuple(out.shape) == (T, self.hidden)
+        for t in (x, topk_ids, topk_w, shared_w, out):
+            assert t is None or t.device == dev, "all tensors on the layer's device"
+        return T, k
+
     def __call__(self, x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor,
                  shared_w: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
                  workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
-        T = x.shape[0]
-        k = topk_ids.shape[1]
-        assert x.dtype == torch.bfloat16 and x.is_contiguous() and topk_ids.dtype == torch.int32
-        assert topk_w.dtype == torch.float32
+        T, k = self._check_args(x, topk_ids, topk_w, shared_w, out)
         if out is None:
             out = torch.empty(T, self.hidden, dtype=torch.bfloat16, device=x.device)
         ws = workspace if workspace is not None else self.workspace(T, k)
         check(load().mxm_moe_group_gemm(self._h, _ptr(x), T, k, _ptr(topk_ids), _ptr(topk_w), _ptr(shared_w),
                                         _ptr(out), _ptr(ws), ws.numel(), _stream()))
         return out
+
+    # ---------------------------------------------------------------- test-only introspection
+    def workspace_layout(self, T: int, top_k: int) -> dict:
+        """Byte offsets of the hot path's intermediate buffers (mxm_debug_workspace_layout; -1 = absent)."""
+        off = (C.c_int64 * len(_lib.WS_NAMES))()
+        check(load().mxm_debug_workspace_layout(self._h, T, top_k, off))
+        return {n: int(off[i]) for i, n in enumerate(_lib.WS_NAMES)}
+
+    def call_dump(self, x, topk_ids, topk_w, shared_w=None):
+        """mxm_moe_group_gemm through the accumulator-dump kernel: (y, workspace, acc_gu, acc_down).
+
+        acc_gu int32 [2, hidden/128, R, F] (gate, up), acc_down int32 [F/128, R, hidden]; raw 32-bit words.
+        """
+        T, k = self._check_args(x, topk_ids, topk_w, shared_w, None)
+        nb = C.c_int64()
+        check(load().mxm_debug_acc_bytes(self._h, T, k, C.byref(nb)))
+        lay = self.workspace_layout(T, k)
+        R, F, d = lay["R"], lay["f_max"], self.hidden
+        acc = torch.zeros(nb.value // 4, dtype=torch.int32, device=x.device)
+        ws = torch.zeros(self.workspace_bytes(T, k), dtype=torch.uint8, device=x.device)
+        y = torch.empty(T, self.hidden, dtype=torch.bfloat16, device=x.device)
+        check(load().mxm_debug_moe_group_gemm_dump(self._h, _ptr(x), T, k, _ptr(topk_ids), _ptr(topk_w),
+                                                   _ptr(shared_w), _ptr(y), _ptr(ws), ws.numel(), _ptr(acc),
+                                                   nb.value, _stream()))
+        n_gu = 2 * (d // 128) * R * F
+        return y, ws, acc[:n_gu].view(2, d // 128, R, F), acc[n_gu:].view(F // 128, R, d)
 
     def profile(self, n_slots: int):
         """Record per-stage CUDA events for the next calls (ring of n_slots calls)."""

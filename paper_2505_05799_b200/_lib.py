@@ -12,6 +12,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmxmoe.so")
 
 MXM_OK, MXM_E_CONFIG, MXM_E_DATA, MXM_E_CUDA, MXM_E_NCCL = 0, 3, 4, 5, 6
+# include/mxmoe.h MXM_WS_* (workspace introspection, test-only)
+WS_NAMES = ["row_src", "row_w", "row_exp", "inv", "xb", "xqa", "xsa", "xqb", "xsb", "h", "hq", "hs", "o", "v_off",
+            "R", "f_max", "xca", "xcb", "hc"]
 
 
 class MxmError(RuntimeError):
@@ -63,6 +66,9 @@ SIGNATURES = {
     "mxm_ep_route": (C.c_int, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P]),
     "mxm_ep_pack": (C.c_int, [_P, _I64, _I32, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "mxm_ep_combine": (C.c_int, [_P, _P, _P, _I32, _I64, _I32, _P, _P, _P]),
+    "mxm_debug_workspace_layout": (C.c_int, [_P, _I64, _I32, C.POINTER(_I64)]),
+    "mxm_debug_acc_bytes": (C.c_int, [_P, _I64, _I32, C.POINTER(_I64)]),
+    "mxm_debug_moe_group_gemm_dump": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _I64, _P, _I64, _P]),
     "mxm_last_error": (C.c_char_p, []),
     "mxm_version": (C.c_char_p, []),
 }

@@ -21,10 +21,20 @@ __device__ __forceinline__ int warp_sum(int v) {
   return v;
 }
 
+// Code byte of an integer code q (|q| <= 127): two's complement int8 (kind::i8 operands, canonical output), or
+// for E4 the e4m3 byte (q<0)<<7 | |q| whose value is q * 2^-9 (|q| <= 15; kind::f8f6f4 operands of w4a4 blocks).
+template <bool E4>
+__device__ __forceinline__ uint32_t code_byte(int q) {
+  if constexpr (E4)
+    return (q < 0 ? 0x80u : 0u) | (uint32_t)(q < 0 ? -q : q);
+  else
+    return (uint32_t)q & 0xFFu;
+}
+
 // Quantize `n` bf16 values src[0..n) (n % 256 == 0 or n == 128: each lane handles 4- or 8-element
 // vectors) into dst codes, return the group scale; whole warp participates.
 // src may be global (generic pointer). Uses 8-byte (4 x bf16) vector loads.
-template <bool kCoherent = false>
+template <bool kCoherent = false, bool E4 = false>
 __device__ __forceinline__ float quant_group_warp(const uint16_t* src, int8_t* __restrict__ dst, int n, int qmax,
                                                   int* qsum_out) {
   const int lane = threadIdx.x & 31;
@@ -55,7 +65,7 @@ __device__ __forceinline__ float quant_group_warp(const uint16_t* src, int8_t* _
       q = fminf(fmaxf(q, -fq), fq);
       int qi = (int)q;
       qs += qi;
-      packed |= (uint32_t)(qi & 0xFF) << (8 * j);
+      packed |= code_byte<E4>(qi) << (8 * j);
     }
     *reinterpret_cast<uint32_t*>(dst + i) = packed;
   }
@@ -66,10 +76,12 @@ __device__ __forceinline__ float quant_group_warp(const uint16_t* src, int8_t* _
 // One whole row of d bf16 values (d % 128 == 0, d <= 128 * MAXG) quantized by one warp in groups of g
 // (128, or g == d for per-token scales): the row is loaded once into registers (lane l holds elements
 // 128*i + 4l .. +3 of chunk i), all loads in flight together; same arithmetic as quant_group_warp.
-// Scales go to sc[gi * R] (group-major [g][R]).
-template <int MAXG>
+// Scales go to sc[gi * R], code sums (if qs != nullptr) to qs[gi * R] (group-major [g][R]).
+// The hot path's gate/up input quantizer (route.cu gather) and the mxm_act_quant debug entry both call it.
+template <int MAXG, bool E4>
 __device__ __forceinline__ void quant_row_warp(const uint16_t* __restrict__ src, int8_t* __restrict__ dst, int d, int g,
-                                               int qmax, float* __restrict__ sc, int64_t R) {
+                                               int qmax, float* __restrict__ sc, int32_t* __restrict__ qs,
+                                               int64_t R) {
   const int lane = threadIdx.x & 31;
   const int nch = d / 128;
   uint2 v[MAXG];
@@ -81,7 +93,7 @@ __device__ __forceinline__ void quant_row_warp(const uint16_t* __restrict__ src,
                  fmaxf(fabsf(bf16_bits_to_float(x.y & 0xFFFFu)), fabsf(bf16_bits_to_float(x.y >> 16))));
   };
   const float fq = (float)qmax;
-  auto quant4 = [&](uint2 x, float r) {
+  auto quant4 = [&](uint2 x, float r, int& qsum) {
     const float f[4] = {bf16_bits_to_float(x.x & 0xFFFFu), bf16_bits_to_float(x.x >> 16),
                         bf16_bits_to_float(x.y & 0xFFFFu), bf16_bits_to_float(x.y >> 16)};
     uint32_t packed = 0;
@@ -89,7 +101,8 @@ __device__ __forceinline__ void quant_row_warp(const uint16_t* __restrict__ src,
     for (int j = 0; j < 4; ++j) {
       float q = rintf(__fmul_rn(f[j], r));
       q = fminf(fmaxf(q, -fq), fq);
-      packed |= (uint32_t)((int)q & 0xFF) << (8 * j);
+      qsum += (int)q;
+      packed |= code_byte<E4>((int)q) << (8 * j);
     }
     return packed;
   };
@@ -103,8 +116,13 @@ __device__ __forceinline__ void quant_row_warp(const uint16_t* __restrict__ src,
           r = __fdiv_rn(fq, amax);
           s = __fdiv_rn(amax, fq);
         }
-        *reinterpret_cast<uint32_t*>(dst + 128 * i + 4 * lane) = quant4(v[i], r);
-        if (lane == 0) sc[(int64_t)i * R] = s;
+        int qsum = 0;
+        *reinterpret_cast<uint32_t*>(dst + 128 * i + 4 * lane) = quant4(v[i], r, qsum);
+        if (qs) qsum = warp_sum(qsum);
+        if (lane == 0) {
+          sc[(int64_t)i * R] = s;
+          if (qs) qs[(int64_t)i * R] = qsum;
+        }
       }
     }
   } else {  // per token: one group = the row
@@ -118,10 +136,15 @@ __device__ __forceinline__ void quant_row_warp(const uint16_t* __restrict__ src,
       r = __fdiv_rn(fq, amax);
       s = __fdiv_rn(amax, fq);
     }
+    int qsum = 0;
 #pragma unroll
     for (int i = 0; i < MAXG; ++i)
-      if (i < nch) *reinterpret_cast<uint32_t*>(dst + 128 * i + 4 * lane) = quant4(v[i], r);
-    if (lane == 0) sc[0] = s;
+      if (i < nch) *reinterpret_cast<uint32_t*>(dst + 128 * i + 4 * lane) = quant4(v[i], r, qsum);
+    if (qs) qsum = warp_sum(qsum);
+    if (lane == 0) {
+      sc[0] = s;
+      if (qs) qs[0] = qsum;
+    }
   }
 }
 

@@ -61,15 +61,19 @@ bool encode_2d(CUtensorMap* m, const void* base, bool bf16, uint64_t cols, uint6
   return r == CUDA_SUCCESS;
 }
 
+// SM count of the current device (cached per device ordinal)
 int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = kNumSms;
+  static std::mutex mu;
+  static int n[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kNumSms;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : kNumSms;
   }
-  return n;
+  return n[dev];
 }
 
 int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
@@ -77,6 +81,7 @@ int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
 struct mxm_layer {
   int E, S, V, d, f, fs, f_max;
+  int device;  // CUDA device of the descriptor table (calls must run with it current)
   std::vector<ExpertDesc> ex;
   ExpertDesc* ex_dev;
   bool need_xb, need_xqa, need_xqb, need_hq;
@@ -104,6 +109,7 @@ struct WsLayout {
   int64_t R, g_max, task_cap;
   int64_t err, route_scratch, counts, v_off, row_src, row_w, row_exp, inv;
   int64_t Xb, XqA, XsA, XqB, XsB, H, Hq, Hs, hmax, O;
+  int64_t XcA, XcB, Hc;  // per-(group, row) code sums of e4m3-coded (w4a4) inputs, group-major [g][R] int32
   int64_t tasks, meta, grp_n1, grp_nq, p1_done, hq_done, P, red_cnt;
   int64_t total;
 };
@@ -137,6 +143,9 @@ static WsLayout make_layout(const mxm_layer* l, int64_t T, int k) {
   w.Hq = l->need_hq ? take(R * l->f_max) : -1;
   w.Hs = l->need_hq ? take(4 * R * (l->f_max / 128)) : -1;
   w.hmax = l->need_hq ? take(4 * R) : -1;
+  w.XcA = l->need_xqa ? take(4 * R * (l->d / 128)) : -1;
+  w.XcB = l->need_xqb ? take(4 * R * (l->d / 128)) : -1;
+  w.Hc = l->need_hq ? take(4 * R * (l->f_max / 128)) : -1;
   w.O = take(2 * R * l->d);
   w.tasks = take(16 * w.task_cap);
   w.meta = take(4 * (8 + 4 * w.g_max));
@@ -322,6 +331,7 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
     return cuda_fail(ce, "cudaMemcpy(desc)");
   }
   l->ex_dev = reinterpret_cast<ExpertDesc*>(desc_dev);
+  cudaGetDevice(&l->device);
   *out = l;
   return MXM_OK;
 }
@@ -334,14 +344,23 @@ mxm_status mxm_workspace_bytes(const mxm_layer* l, int64_t max_tokens, int32_t t
   return MXM_OK;
 }
 
-mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int32_t k, const int32_t* topk_ids,
-                              const float* topk_w, const float* shared_w, void* y, void* ws, int64_t ws_bytes,
-                              mxm_stream stream) {
+}  // extern "C"
+
+// The launch sequence of one MoE block; `dump` != nullptr selects the test-only accumulator-dump kernel
+// (mxm_debug_moe_group_gemm_dump) and disables split-K so every accumulator is a whole-K (or whole-group) sum.
+static mxm_status run_group_gemm(const mxm_layer* l, const void* x, int64_t T, int32_t k, const int32_t* topk_ids,
+                                 const float* topk_w, const float* shared_w, void* y, void* ws, int64_t ws_bytes,
+                                 mxm_stream stream, uint32_t* dump) {
   if (!l || !ws || (T > 0 && (!x || !topk_ids || !topk_w || !y))) return fail(MXM_E_CONFIG, "null argument");
   if (k <= 0 || k > 32 || T < 0) return fail(MXM_E_CONFIG, "bad top_k / T");
   const WsLayout w = make_layout(l, T, k);
   if (ws_bytes < w.total) return fail(MXM_E_CONFIG, "workspace too small");
   if (w.R >= (1LL << 31) || w.task_cap >= (1LL << 31)) return fail(MXM_E_CONFIG, "too many tokens");
+  {
+    int dev = -1;
+    MXM_CUDA(cudaGetDevice(&dev));
+    if (dev != l->device) return fail(MXM_E_CONFIG, "layer was initialised on another device");
+  }
   if (T == 0) return MXM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* b = reinterpret_cast<uint8_t*>(ws);
@@ -380,11 +399,12 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   MXM_CUDA(cudaStreamWaitEvent(ml->side, ml->ev_fork, 0));
   MXM_CUDA(launch_plan(l->ex_dev, l->V, l->E, T, l->d, v_off, (int)w.g_max, w.task_cap, (Task*)P(w.tasks),
                        (int32_t*)P(w.meta), (int32_t*)P(w.grp_n1), (int32_t*)P(w.grp_nq), (int32_t*)P(w.p1_done),
-                       (int32_t*)P(w.hq_done), (int32_t*)P(w.red_cnt), ml->side));
+                       (int32_t*)P(w.hq_done), dump ? nullptr : (int32_t*)P(w.red_cnt), ml->side));
   MXM_CUDA(cudaEventRecord(ml->ev_join, ml->side));
   // S2 activation quantize + gather
   MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
-                               (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), (uint32_t*)P(w.hmax), st));
+                               (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), (int32_t*)P(w.XcA), (int32_t*)P(w.XcB),
+                               (uint32_t*)P(w.hmax), st));
   mark(2);
   MXM_CUDA(cudaStreamWaitEvent(st, ml->ev_join, 0));
   mark(3);  // the plan's time beyond the gather's (usually ~0)
@@ -411,6 +431,10 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   prm.xs[0] = nullptr;
   prm.xs[1] = (const float*)P(w.XsA);
   prm.xs[2] = (const float*)P(w.XsB);
+  prm.xc[0] = nullptr;
+  prm.xc[1] = (const int32_t*)P(w.XcA);
+  prm.xc[2] = (const int32_t*)P(w.XcB);
+  prm.Hc = (int32_t*)P(w.Hc);
   prm.H = (uint16_t*)P(w.H);
   prm.Hq = (int8_t*)P(w.Hq);
   prm.Hs = (float*)P(w.Hs);
@@ -418,8 +442,9 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   prm.hmax = (uint32_t*)P(w.hmax);
   prm.O = (uint16_t*)P(w.O);
   prm.row_w = row_w;
-  prm.P = (float*)P(w.P);
-  prm.red_cnt = (int32_t*)P(w.red_cnt);
+  prm.P = dump ? nullptr : (float*)P(w.P);
+  prm.red_cnt = dump ? nullptr : (int32_t*)P(w.red_cnt);
+  prm.dump = dump;
   prm.d = l->d;
   prm.f_max = l->f_max;
   prm.prof = reinterpret_cast<unsigned long long*>(l->prof_counters);
@@ -428,6 +453,41 @@ mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int3
   // S8 combine
   MXM_CUDA(launch_combine(P(w.O), l->d, T, k, l->S, inv, y, st));
   mark(5);
+  return MXM_OK;
+}
+
+extern "C" {
+
+mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int32_t k, const int32_t* topk_ids,
+                              const float* topk_w, const float* shared_w, void* y, void* ws, int64_t ws_bytes,
+                              mxm_stream stream) {
+  return run_group_gemm(l, x, T, k, topk_ids, topk_w, shared_w, y, ws, ws_bytes, stream, nullptr);
+}
+
+mxm_status mxm_debug_acc_bytes(const mxm_layer* l, int64_t T, int32_t k, int64_t* bytes) {
+  if (!l || !bytes || T < 0 || k <= 0 || k > 32) return fail(MXM_E_CONFIG, "bad argument");
+  // gate / up: [2][d/128][R][f_max]; down: [f_max/128][R][d]  (uint32)
+  const int64_t R = make_layout(l, T, k).R;
+  *bytes = (int64_t)4 * (2 * (l->d / 128) * R * l->f_max + (l->f_max / 128) * R * l->d);
+  return MXM_OK;
+}
+
+mxm_status mxm_debug_moe_group_gemm_dump(const mxm_layer* l, const void* x, int64_t T, int32_t k,
+                                         const int32_t* topk_ids, const float* topk_w, const float* shared_w, void* y,
+                                         void* ws, int64_t ws_bytes, void* acc, int64_t acc_bytes, mxm_stream stream) {
+  int64_t need = 0;
+  mxm_status s = mxm_debug_acc_bytes(l, T, k, &need);
+  if (s != MXM_OK) return s;
+  if (!acc || acc_bytes < need) return fail(MXM_E_CONFIG, "accumulator dump buffer too small");
+  return run_group_gemm(l, x, T, k, topk_ids, topk_w, shared_w, y, ws, ws_bytes, stream, (uint32_t*)acc);
+}
+
+mxm_status mxm_debug_workspace_layout(const mxm_layer* l, int64_t T, int32_t k, int64_t* off) {
+  if (!l || !off || T < 0 || k <= 0 || k > 32) return fail(MXM_E_CONFIG, "bad argument");
+  const WsLayout w = make_layout(l, T, k);
+  const int64_t v[MXM_WS_N] = {w.row_src, w.row_w, w.row_exp, w.inv, w.Xb, w.XqA, w.XsA, w.XqB, w.XsB,
+                               w.H, w.Hq, w.Hs, w.O, w.v_off, w.R, l->f_max, w.XcA, w.XcB, w.Hc};
+  for (int i = 0; i < MXM_WS_N; ++i) off[i] = v[i];
   return MXM_OK;
 }
 

@@ -19,12 +19,20 @@ constexpr int kRowsPerTile = 128;  // output channels per tile (UMMA M)
 enum Kind : int8_t {
   KIND_W16 = 0,     // F16 image chunks (bf16 pass-through)
   KIND_WO = 1,      // F16 row-word chunks, weight-only w2/w3/w4/w8 -> dequant to bf16
-  KIND_WA_ROW = 2,  // I8 row-word chunks, w4a4 / w5a5 -> unpack to s8
-  KIND_WA_IMG = 3,  // I8 image chunks, w8a8
+  KIND_WA_ROW = 2,  // I8 row-word chunks, w5a5 -> unpack to s8, tcgen05 kind::i8
+  KIND_WA_IMG = 3,  // I8 image chunks, w8a8, tcgen05 kind::i8
+  KIND_WA_F8 = 4,   // I8 row-word chunks (same bytes as KIND_WA_ROW w4), w4a4 -> nibble bytes read as e4m3 by
+                    // tcgen05 kind::f8f6f4: byte u in [0,15] is the e4m3 value u * 2^-9 (subnormal / first binade,
+                    // linear in u), activation codes are e4m3 (q<0)<<7 | |q| = q * 2^-9, so the f32 accumulator
+                    // is 2^-18 * sum (q_w + 8) q_a exactly (integer sums < 2^24; tools/probe_f8.cu)
 };
 
-__host__ __device__ inline bool kind_is_i8(int k) { return k >= KIND_WA_ROW; }
-__host__ __device__ inline bool kind_needs_transform(int k) { return k == KIND_WO || k == KIND_WA_ROW; }
+// weight-activation kinds: 8-bit MMA operands, 128-element K stages, per-group / per-channel scale drains
+__host__ __device__ inline bool kind_is_wa(int k) { return k >= KIND_WA_ROW; }
+__host__ __device__ inline bool kind_is_f8(int k) { return k == KIND_WA_F8; }
+// row-word packed 8-bit-operand kinds (nibble + bit planes, unpacked by the transform warps)
+__host__ __device__ inline bool kind_is_row8(int k) { return k == KIND_WA_ROW || k == KIND_WA_F8; }
+__host__ __device__ inline bool kind_needs_transform(int k) { return k == KIND_WO || kind_is_row8(k); }
 
 // Geometry of one packed linear block W[N, K].
 struct PackGeom {
@@ -86,7 +94,7 @@ constexpr int kSplitRows = 512;  // split only when the launch has <= this many 
 __host__ __device__ inline int task_tile(const Task& t) { return t.phase == 2 ? (t.ntile & 0x3FF) : t.ntile; }
 __host__ __device__ inline int task_slice(const Task& t) { return t.phase == 2 ? (t.ntile >> 10) : 0; }
 __host__ __device__ inline bool down_splittable(const ExpertDesc& e) {
-  return !(kind_is_i8(e.blk[2].geo.kind) && e.blk[2].geo.group == 128);  // g128 W-A downs drain per group
+  return !(kind_is_wa(e.blk[2].geo.kind) && e.blk[2].geo.group == 128);  // g128 W-A downs drain per group
 }
 // stage range [ks0, ks1) of slice `sl` of S over ns stages (slices of an even number of stages so a g128 / g64
 // weight-only group never straddles two slices)
@@ -100,13 +108,13 @@ __host__ __device__ inline void split_range(int ns, int S, int sl, int& ks0, int
 // accumulator buffer (2 x 160 columns next to a 3-slot A ring); register-accumulated tiles (g128 W-A dual, or gate and up as two sub-loops) keep
 // 64 columns per warpgroup half in registers -> 64 tokens.
 __host__ __device__ inline int tile_cap(const ExpertDesc& e) {
-  const bool reg = !e.dual || (kind_is_i8(e.blk[0].geo.kind) && e.blk[0].geo.group == 128);
+  const bool reg = !e.dual || (kind_is_wa(e.blk[0].geo.kind) && e.blk[0].geo.group == 128);
   return reg ? 64 : MXM_DUAL_TILE;
 }
 // Down tasks pair two 128-channel output tiles (two mats sharing the h tile) unless the down is a g128
 // W-A block whose register-accumulated drain would exceed 64 columns per thread.
 __host__ __device__ inline bool down_pair(const ExpertDesc& e, int nt, int nd) {
-  const bool g128 = kind_is_i8(e.blk[2].geo.kind) && e.blk[2].geo.group == 128;
+  const bool g128 = kind_is_wa(e.blk[2].geo.kind) && e.blk[2].geo.group == 128;
   return nd >= 2 && !(g128 && nt > 64);
 }
 __host__ __device__ inline int down_tasks(const ExpertDesc& e, int nt, int nd) {
@@ -141,7 +149,7 @@ __host__ __device__ inline mxm_status make_geom(const mxm_scheme& s, int64_t N, 
     if (s.a_bits != s.w_bits || !s.symmetric) return MXM_E_CONFIG;
     if (!(s.w_bits == 4 || s.w_bits == 5 || s.w_bits == 8)) return MXM_E_CONFIG;
     if (!(s.w_group == -1 || s.w_group == 128) || s.a_group != s.w_group) return MXM_E_CONFIG;
-    r.kind = s.w_bits == 8 ? KIND_WA_IMG : KIND_WA_ROW;
+    r.kind = s.w_bits == 8 ? KIND_WA_IMG : (s.w_bits == 4 ? KIND_WA_F8 : KIND_WA_ROW);
     r.ks = 128;
     r.group = s.w_group == -1 ? (int32_t)K : s.w_group;
   }
@@ -152,7 +160,7 @@ __host__ __device__ inline mxm_status make_geom(const mxm_scheme& s, int64_t N, 
   const int64_t ng = K / r.group;
   r.rb_bytes = (int64_t)r.ns * r.code_bytes + (r.kind == KIND_WO ? ng * r.meta_bytes : 0);
   r.wa_scale_off = (N / 128) * r.rb_bytes;
-  r.total_bytes = r.wa_scale_off + (kind_is_i8(r.kind) ? ng * N * 2 : 0);
+  r.total_bytes = r.wa_scale_off + (kind_is_wa(r.kind) ? ng * N * 2 : 0);
   *g = r;
   return MXM_OK;
 }

@@ -19,6 +19,7 @@
 // group"), ping-ponging between TMEM buffers so the tensor core keeps running.
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <mutex>
 #include <type_traits>
 
 #include "actq.cuh"
@@ -55,7 +56,8 @@ constexpr int kCtlBytes = 8192;
 // array, from the 16-byte-aligned floor) next to the stage's operands; the epilogue drains the event's
 // accumulator against them, then releases the slot.
 constexpr int kSSlots = 4;
-constexpr int kSSlotBytes = 1024;  // [0,256) mat-0 s_w | [256,512) mat-1 s_w | [512,1024) s_a (<= 125 floats)
+// [0,256) mat-0 s_w | [256,512) mat-1 s_w | [512,1024) s_a (<= 125 floats) | [1024,1536) code sums (w4a4)
+constexpr int kSSlotBytes = 1536;
 constexpr int kOffScale = kOffCtl + kCtlBytes;
 constexpr int kSmemBytes = kOffScale + kSSlots * kSSlotBytes + 1024;
 
@@ -69,15 +71,18 @@ struct Ctl {
   uint32_t tmem_base;
   int red_last;  // split-K: this CTA's slice arrived last (epilogue broadcast)
   uint32_t colmax[2][2][4][8];  // [buffer][warpgroup][lane quarter][column] for the fused g128 h-quant
-  alignas(16) float cw[8][2][64];  // per epilogue warp: [0] activation scale of the current drain event,
-                                   // [1] route weight of this warp's token columns (broadcast reads)
+  alignas(16) float cw[8][3][64];  // per epilogue warp and token column (broadcast reads): [0] activation scale
+                                   // of the current drain event (w4a4: s_a * 2^18), [1] route weight,
+                                   // [2] w4a4 offset correction -8 s_a sum(q_a) of the event
+  int32_t colsum[2][2][4][8];      // [buffer][warpgroup][lane quarter][column]: fused g128 h-quant code sums (w4a4)
 };
 static_assert(sizeof(Ctl) <= kCtlBytes, "ctl");
 
 struct SubLoop {
   const LinDesc* mat[2];
   int tile[2];                           // 128-channel output tile of each mat
-  int nmats, bmap, ns, i8, xform, g128;  // xform: bit m set = mat m needs the packed->A transform
+  int nmats, bmap, ns, i8, f8, xform, g128;  // i8: W-A (8-bit operands); f8: w4a4 on kind::f8f6f4 (common.cuh)
+                                              // xform: bit m set = mat m needs the packed->A transform
   int ks0, ks1;                           // stage range (a split-K slice of a down task, else [0, ns))
 };
 
@@ -90,7 +95,8 @@ __device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, i
   s.nmats = b ? 2 : 1;
   s.bmap = bmap;
   s.ns = a->geo.ns;
-  s.i8 = kind_is_i8(a->geo.kind);
+  s.i8 = kind_is_wa(a->geo.kind);
+  s.f8 = kind_is_f8(a->geo.kind);
   s.xform = (kind_needs_transform(a->geo.kind) ? 1 : 0) | ((b && kind_needs_transform(b->geo.kind)) ? 2 : 0);
   s.g128 = s.i8 && a->geo.group == 128;
   s.ks0 = 0;
@@ -286,6 +292,19 @@ __device__ __forceinline__ void xform_wo_any(int bits, const uint8_t* raw, bool 
 __device__ __forceinline__ uint32_t to_s8_4(uint32_t u, uint32_t bias) { return (u + bias) ^ 0x80808080u; }
 
 // W-A w4/w5 unpack of one half-stage of one row: 64 of the stage's 128 codes -> s8, o[j] = bytes 4j..4j+3
+// w4a4 (kind::f8f6f4) unpack of one half-stage of one row: the offset-binary nibbles u = q + 8 zero-extended
+// to bytes, which the MMA reads as the e4m3 values u * 2^-9 (common.cuh KIND_WA_F8): one AND per 4 codes
+template <int H>
+__device__ __forceinline__ void xform_f8(const uint8_t* __restrict__ raw, int r, uint32_t (&o)[16]) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(raw);
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const uint32_t word = w[(8 * H + jj) * 128 + r];
+    o[2 * jj] = word & 0x0F0F0F0Fu;
+    o[2 * jj + 1] = (word >> 4) & 0x0F0F0F0Fu;
+  }
+}
+
 template <int BITS, int H>
 __device__ __forceinline__ void xform_wa(const uint8_t* __restrict__ raw, int r, uint32_t (&o)[16]) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(raw);
@@ -315,13 +334,22 @@ __device__ __forceinline__ void xform_stage(const SubLoop& s, const uint8_t* x0,
                                             bool hmA, bool hmB, int bitsA, int bitsB, int mbA, int mbB, bool symA,
                                             bool symB, uint32_t offA, uint32_t offB, bool xa, bool xb, uint32_t& sa,
                                             uint32_t& za, uint32_t& sb, uint32_t& zb, uint32_t (&o)[16]) {
-  if (s.i8) {
+  if (s.f8) {
     if (xa) {
-      if (bitsA == 4) xform_wa<4, H>(x0, r, o); else xform_wa<5, H>(x0, r, o);
+      xform_f8<H>(x0, r, o);
       tmem_st16(tA + 16 * H, o);
     }
     if (xb) {
-      if (bitsB == 4) xform_wa<4, H>(x1, r, o); else xform_wa<5, H>(x1, r, o);
+      xform_f8<H>(x1, r, o);
+      tmem_st16(tA + 32 + 16 * H, o);
+    }
+  } else if (s.i8) {
+    if (xa) {
+      xform_wa<5, H>(x0, r, o);
+      tmem_st16(tA + 16 * H, o);
+    }
+    if (xb) {
+      xform_wa<5, H>(x1, r, o);
       tmem_st16(tA + 32 + 16 * H, o);
     }
   } else {
@@ -378,7 +406,9 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // (IADD + FADD on the full-rate pipes instead of the quarter-rate I2F).
 // I8 / TWO / SMALL are template parameters: with run-time flags the compiler if-converts both conversion
 // paths and the mat-1 work into predicated instructions that still take issue slots
-template <int HALF, int DST0, bool I8, bool TWO, bool SMALL>
+// F8 (w4a4, kind::f8f6f4): the accumulator is f32 = 2^-18 sum (q_w + 8) q_a exactly; with a = s_a 2^18 and
+// b = -8 s_a sum(q_a) per token column (sa[], sa[128 + col]) the event adds s_w * (acc * a + b): two FFMA2, no I2F.
+template <int HALF, int DST0, bool I8, bool TWO, bool SMALL, bool F8 = false>
 __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, float sw0, float sw1,
                                             const float* sa) {
   constexpr int CH = 8;  // 16-wide staging + 64 accumulators exceeds the 128-register epilogue budget (spills)
@@ -412,7 +442,22 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
       }
     } else
 #endif
-    if constexpr (I8) {
+    if constexpr (I8 && F8) {
+#pragma unroll
+      for (int j = 0; j < CH; j += 2) {
+        const int col = c0 + j;
+        const float4 sa4 = *reinterpret_cast<const float4*>(sa + (col & ~3));  // 16-B aligned, broadcast
+        const float4 sb4 = *reinterpret_cast<const float4*>(sa + 128 + (col & ~3));
+        const float2 sac = (col & 2) ? make_float2(sa4.z, sa4.w) : make_float2(sa4.x, sa4.y);
+        const float2 sbc = (col & 2) ? make_float2(sb4.z, sb4.w) : make_float2(sb4.x, sb4.y);
+        const float2 fa = make_float2(__uint_as_float(va[cur][j]), __uint_as_float(va[cur][j + 1]));
+        acc2[DST0 + col / 2] = ffma2(ffma2(fa, sac, sbc), make_float2(sw0, sw0), acc2[DST0 + col / 2]);
+        if constexpr (TWO) {
+          const float2 fb = make_float2(__uint_as_float(vb[cur][j]), __uint_as_float(vb[cur][j + 1]));
+          acc2[16 + col / 2] = ffma2(ffma2(fb, sac, sbc), make_float2(sw1, sw1), acc2[16 + col / 2]);
+        }
+      }
+    } else if constexpr (I8) {
 #pragma unroll
       for (int j = 0; j < CH; j += 2) {
         const int col = c0 + j;
@@ -466,42 +511,48 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
 #endif
 }
 
-template <int DST0, bool I8, bool TWO, bool SMALL>
+template <int DST0, bool I8, bool TWO, bool SMALL, bool F8>
 __device__ __forceinline__ void drain_half(int half, float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, float sw0,
                                            float sw1, const float* sa) {
   // two mats: tiles of <= 64 tokens (half <= 32). One mat: also a g128 W-A down of an expert whose gate/up
   // allow 96-token tiles (single-mat down, half 48); half 64 keeps the 128-token case total
   if (half == 8) {
-    drain_event<8, DST0, I8, TWO, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+    drain_event<8, DST0, I8, TWO, SMALL, F8>(acc2, addrA, addrB, sw0, sw1, sa);
   } else if (half == 16) {
-    drain_event<16, DST0, I8, TWO, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+    drain_event<16, DST0, I8, TWO, SMALL, F8>(acc2, addrA, addrB, sw0, sw1, sa);
   } else if (half == 32 || TWO || DST0 != 0) {
-    drain_event<32, DST0, I8, TWO, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+    drain_event<32, DST0, I8, TWO, SMALL, F8>(acc2, addrA, addrB, sw0, sw1, sa);
   } else if constexpr (!TWO && DST0 == 0) {
     if (half == 40)
-      drain_event<40, 0, I8, false, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+      drain_event<40, 0, I8, false, SMALL, F8>(acc2, addrA, addrB, sw0, sw1, sa);
     else if (half == 48)
-      drain_event<48, 0, I8, false, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+      drain_event<48, 0, I8, false, SMALL, F8>(acc2, addrA, addrB, sw0, sw1, sa);
     else
-      drain_event<64, 0, I8, false, SMALL>(acc2, addrA, addrB, sw0, sw1, sa);
+      drain_event<64, 0, I8, false, SMALL, F8>(acc2, addrA, addrB, sw0, sw1, sa);
   }
 }
 
 // i8 && small: W-A g128 events (dual or single mat); i8 && !small / bf16: one mat of a heterogeneous
-// gate/up pair (never two mats)
+// gate/up pair (never two mats). f8: w4a4 (kind::f8f6f4 accumulators, drain_event F8)
 template <int DST0>
 __device__ __forceinline__ void drain_event_any(int half, float2 (&acc2)[32], uint32_t addrA, uint32_t addrB, bool i8,
-                                                bool two, bool small, float sw0, float sw1, const float* sa) {
-  if (i8 && small) {
+                                                bool f8, bool two, bool small, float sw0, float sw1, const float* sa) {
+  if (f8) {
     if (two) {
-      if constexpr (DST0 == 0) drain_half<0, true, true, true>(half, acc2, addrA, addrB, sw0, sw1, sa);
+      if constexpr (DST0 == 0) drain_half<0, true, true, true, true>(half, acc2, addrA, addrB, sw0, sw1, sa);
     } else {
-      drain_half<DST0, true, false, true>(half, acc2, addrA, addrB, sw0, sw1, sa);
+      drain_half<DST0, true, false, true, true>(half, acc2, addrA, addrB, sw0, sw1, sa);
+    }
+  } else if (i8 && small) {
+    if (two) {
+      if constexpr (DST0 == 0) drain_half<0, true, true, true, false>(half, acc2, addrA, addrB, sw0, sw1, sa);
+    } else {
+      drain_half<DST0, true, false, true, false>(half, acc2, addrA, addrB, sw0, sw1, sa);
     }
   } else if (i8) {
-    drain_half<DST0, true, false, false>(half, acc2, addrA, addrB, sw0, sw1, sa);
+    drain_half<DST0, true, false, false, false>(half, acc2, addrA, addrB, sw0, sw1, sa);
   } else {
-    drain_half<DST0, false, false, false>(half, acc2, addrA, addrB, sw0, sw1, sa);
+    drain_half<DST0, false, false, false, false>(half, acc2, addrA, addrB, sw0, sw1, sa);
   }
 }
 
@@ -510,10 +561,17 @@ __device__ __forceinline__ void drain_event_any(int half, float2 (&acc2)[32], ui
 // atomicMax (per-token W-A down, quantized later in one pass); 2 fused per-128-group quantization: the group
 // is exactly this tile's 128 channels, so codes + scale are produced here (DESIGN R9).
 // nv = valid columns from colc (rows of the m-tile), hrow = &H[row0 + colc][n] (row stride f_max).
+template <bool DUMP = false>
 __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int dmode, int qmax, int n, int colc, int nv,
                                      const uint16_t (&hb)[8], Ctl& ctl, int wg, int q, int lane, uint32_t& rbuf) {
   const int64_t row0 = (int64_t)t.row0 + colc;
-  if (dmode == 2) {
+  if (dmode >= 2) {  // 2: int8 codes (w5a5 / w8a8 g128 down), 3: e4m3 codes + group code sums (w4a4 g128 down)
+    if constexpr (DUMP) {  // test build: also keep the bf16 h the fused quantizer consumed (bit-exact h-quant test)
+      uint16_t* hrow = p.H + row0 * p.f_max + n;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < nv) hrow[(int64_t)j * p.f_max] = hb[j];
+    }
     uint32_t m[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) m[j] = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(bf16f(hb[j]))));
@@ -535,11 +593,26 @@ __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int 
       if (q == 0 && lane < nv) p.Hs[row0 + lane + (int64_t)t.ntile * p.hs_stride] = sc_l;
     }
     int8_t* hq = p.Hq + row0 * p.f_max + n;
+    int qi[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float r = __shfl_sync(0xffffffffu, r_l, j);
-      const float qv = fminf(fmaxf(rintf(__fmul_rn(bf16f(hb[j]), r)), -fq), fq);
-      if (j < nv) hq[(int64_t)j * p.f_max] = (int8_t)(int)qv;
+      qi[j] = (int)fminf(fmaxf(rintf(__fmul_rn(bf16f(hb[j]), r)), -fq), fq);
+      if (j < nv) hq[(int64_t)j * p.f_max] = (int8_t)(dmode == 3 ? code_byte<true>(qi[j]) : code_byte<false>(qi[j]));
+    }
+    if (dmode == 3) {  // sum of the group's codes per token column: warp sums, then the 4 warps of the warpgroup
+      int cs[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cs[j] = __reduce_add_sync(0xffffffffu, qi[j]);
+      if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ctl.colsum[rbuf][wg][q][j] = cs[j];
+      named_bar_sync(2 + wg, 128);  // (double-buffered by rbuf: the next write of this buffer is 2 barriers away)
+      if (q == 0 && lane < 8 && lane < nv)
+        p.Hc[row0 + lane + (int64_t)t.ntile * p.hs_stride] = ctl.colsum[rbuf][wg][0][lane] +
+                                                              ctl.colsum[rbuf][wg][1][lane] +
+                                                              ctl.colsum[rbuf][wg][2][lane] +
+                                                              ctl.colsum[rbuf][wg][3][lane];
     }
     rbuf ^= 1;
     return;
@@ -553,6 +626,33 @@ __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int 
     for (int j = 0; j < 8; ++j) {
       const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(bf16f(hb[j]))));
       if (lane == 0 && j < nv) atomicMax(p.hmax + row0 + j, m);
+    }
+  }
+}
+
+// Test build only (mxm_debug_moe_group_gemm_dump): copy the raw 32-bit accumulators of one drain event -- this
+// warpgroup's `half` token columns starting at TMEM column addrA (mat 0) / addrB (mat 1) -- to p.dump, before
+// the drain consumes them: gate / up (j = 0, 1) at ((j * d/128 + g) * R + row) * f_max + n, down (j = 2) at
+// 2 * (d/128) * R * f_max + (g * R + row) * d + n.
+__device__ __forceinline__ int64_t dump_index(const GemmParams& p, int j, int g, int64_t row, int n) {
+  const int64_t R = p.hs_stride;
+  const int64_t gu = (int64_t)(p.d / 128) * R * p.f_max;
+  return j < 2 ? (((int64_t)j * (p.d / 128) + g) * R + row) * p.f_max + n : 2 * gu + ((int64_t)g * R + row) * p.d + n;
+}
+__device__ __forceinline__ void dump_event(const GemmParams& p, uint32_t addrA, uint32_t addrB, bool two, int jA,
+                                           int jB, int g, int nA, int nB, int64_t row0, int half, int nvalid) {
+  for (int c = 0; c < half; c += 8) {
+    uint32_t va[8], vb[8];
+    tmem_ld8(addrA + c, va);
+    if (two) tmem_ld8(addrB + c, vb);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (c + j < nvalid) {
+        const int64_t row = row0 + c + j;
+        p.dump[dump_index(p, jA, g, row, nA)] = va[j];
+        if (two) p.dump[dump_index(p, jB, g, row, nB)] = vb[j];
+      }
     }
   }
 }
@@ -584,11 +684,12 @@ __device__ __forceinline__ uint32_t bcast(uint32_t v) { return __shfl_sync(0xfff
 // operands in uniform registers (no per-lane "waterfall" loop around each MMA). The issue queue is shallow,
 // so every instruction between two stages' MMAs is a tensor-core bubble: the smem descriptors are built once
 // per sub-loop and advanced by one add per MMA (start address field += 32 B >> 4 per K step).
-template <bool I8, bool TWO, int MODE>
+// MK: MMA kind 0 = kind::f16 (bf16), 1 = kind::i8 (s8 x s8), 2 = kind::f8f6f4 (e4m3 x e4m3, w4a4)
+template <int MK, bool TWO, int MODE>
 __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tmem, uint32_t ns, uint32_t g128,
                                             uint32_t xform, uint32_t nt, MmaState& st, unsigned long long (&pc)[16],
                                             bool prof_on) {
-  const uint32_t idesc = I8 ? idesc_s8(nt) : idesc_bf16(nt);
+  const uint32_t idesc = MK == 1 ? idesc_s8(nt) : (MK == 2 ? idesc_f8(nt) : idesc_bf16(nt));
   // descriptor words: lo = start>>4 | LBO 1 << 16 ; hi = SBO 1024>>4 | version 1 << 14 | SWIZZLE_128B 2 << 29
   const uint32_t lo0 = ((smem_u32(smem) >> 4) & 0x3FFFu) | (1u << 16);
   constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
@@ -632,7 +733,13 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
       for (int k = 0; k < 4; ++k) {
         const uint32_t acc = (k == 0 && ev_start) ? 0u : 1u;
         const uint64_t bd = desc(blo + 2 * k);
-        if constexpr (I8) {
+        if constexpr (MK == 2) {
+          if (ts0) mma_f8_ts(d0, at0 + k * 8, bd, idesc, acc); else mma_f8(d0, desc(blo + kTileLo + 2 * k), bd, idesc, acc);
+          if constexpr (TWO) {
+            if (ts1) mma_f8_ts(d1, at0 + 32 + k * 8, bd, idesc, acc);
+            else mma_f8(d1, desc(blo + 2 * kTileLo + 2 * k), bd, idesc, acc);
+          }
+        } else if constexpr (MK == 1) {
           if (ts0) mma_i8_ts(d0, at0 + k * 8, bd, idesc, acc); else mma_i8(d0, desc(blo + kTileLo + 2 * k), bd, idesc, acc);
           if constexpr (TWO) {
             if (ts1) mma_i8_ts(d1, at0 + 32 + k * 8, bd, idesc, acc);
@@ -669,23 +776,27 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
   }
 }
 
-template <bool I8, bool TWO>
+template <int MK, bool TWO>
 __device__ __forceinline__ void mma_subloop_mode(Ctl& ctl, uint8_t* smem, uint32_t tmem, uint32_t ns, uint32_t g128,
                                                  uint32_t xform, uint32_t nt, MmaState& st,
                                                  unsigned long long (&pc)[16], bool prof_on) {
   const uint32_t all = TWO ? 3u : 1u;
-  if (xform == 0)
-    mma_subloop<I8, TWO, 0>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
+  if (MK == 2) {  // w4a4 weights are always transformed (TS)
+    mma_subloop<MK, TWO, 1>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
+  } else if (xform == 0)
+    mma_subloop<MK, TWO, 0>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
   else if ((xform & all) == all)
-    mma_subloop<I8, TWO, 1>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
+    mma_subloop<MK, TWO, 1>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
   else
-    mma_subloop<I8, TWO, 2>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
+    mma_subloop<MK, TWO, 2>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
 }
 
 // ---------------------------------------------------------------- the kernel
 // SPLIT: the launch may cut downs into K-slices (tiny T, workspace has the partial buffer). A separate
 // instantiation, so the split-K bookkeeping costs the large-T kernel no registers.
-template <bool SPLIT>
+// DUMP: test-only instantiation that also copies every weight-activation accumulator to p.dump (and the bf16 h
+// of fused-quantized downs to p.H) for the bit-exact accumulator tests; never launched by mxm_moe_group_gemm.
+template <bool SPLIT, bool DUMP>
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   // keep the pointer in the shared window (no uintptr_t round trip) so tile accesses compile to LDS/STS
@@ -783,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         if (t.phase == 2) {
           const ExpertDesc& e = p.ex[t.expert];
           // per-token W-A downs wait for the h-quant pass; all others only for the gate/up tiles
-          const bool wa_pt = kind_is_i8(e.blk[2].geo.kind) && e.blk[2].geo.group != 128;
+          const bool wa_pt = kind_is_wa(e.blk[2].geo.kind) && e.blk[2].geo.group != 128;
           const int* ctr = (wa_pt ? p.hq_done : p.p1_done) + t.gid;
           const int need = wa_pt ? p.grp_nq[t.gid] : p.grp_n1[t.gid];
           const unsigned long long td = prof_on ? clock64() : 0ull;
@@ -849,7 +960,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               const float* asrc = ascale_span(abase, p.hs_stride, ks, t.row0, aoff);
               const uint32_t abytes = ((aoff + t.nt) * 4u + 15u) & ~15u;
               const uint32_t wbytes = 256u * (uint32_t)s.nmats;
-              mbar_arrive_expect_tx(&ctl.sfull[ss], wbytes + abytes);
+              mbar_arrive_expect_tx(&ctl.sfull[ss], wbytes + abytes * (s.f8 ? 2u : 1u));
+              if (s.f8) {  // the group's activation code sums (same group-major layout and alignment as s_a)
+                const int32_t* cbase = t.phase == 0 ? p.xc[s.mat[0]->in_slot] : p.Hc;
+                bulk_load(dst + 1024, cbase + (int64_t)ks * p.hs_stride + t.row0 - aoff, abytes, &ctl.sfull[ss]);
+              }
               const uint8_t* w0 = s.mat[0]->packed + g0.wa_scale_off + ((int64_t)ks * g0.N + s.tile[0] * 128) * 2;
               bulk_load(dst, w0, 256u, &ctl.sfull[ss]);
               if (s.nmats == 2) {
@@ -891,21 +1006,26 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         const SubLoop s = sl[si];
         const uint32_t ns = bcast((uint32_t)(SPLIT ? s.ks1 - s.ks0 : s.ns)), g128 = bcast((uint32_t)s.g128);
         const uint32_t xf = bcast((uint32_t)s.xform);
-        const uint32_t i8 = bcast((uint32_t)s.i8), two = bcast((uint32_t)(s.nmats == 2));
+        const uint32_t i8 = bcast((uint32_t)s.i8), f8 = bcast((uint32_t)s.f8), two = bcast((uint32_t)(s.nmats == 2));
         MmaState st{stage, sphase, abuf, acc_ph, aidx, ntr_m};
 #if defined(MXM_PROF_SUBLOOP) && defined(MXM_DEBUG_COUNTERS)
         const unsigned long long t_sl = prof_on ? clock64() : 0ull;
 #endif
-        if (i8) {
+        if (f8) {
           if (two)
-            mma_subloop_mode<true, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+            mma_subloop_mode<2, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
           else
-            mma_subloop_mode<true, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+            mma_subloop_mode<2, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+        } else if (i8) {
+          if (two)
+            mma_subloop_mode<1, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+          else
+            mma_subloop_mode<1, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
         } else {
           if (two)
-            mma_subloop_mode<false, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+            mma_subloop_mode<0, true>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
           else
-            mma_subloop_mode<false, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
+            mma_subloop_mode<0, false>(ctl, smem, tm, ns, g128, xf, nt, st, pc, prof_on);
         }
 #if defined(MXM_PROF_SUBLOOP) && defined(MXM_DEBUG_COUNTERS)
         if (prof_on) pc[12] += clock64() - t_sl;
@@ -1047,6 +1167,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           // latency-bound at a few GB/s per SM)
           constexpr int kU = 8;
           const int n8 = K / 8;
+          const bool e4 = kind_is_f8(L.geo.kind);  // w4a4 down: e4m3 codes + the row's code sum
+          int qsum = 0;
           for (int i0 = lane; i0 < n8; i0 += 32 * kU) {
             uint4 v[kU];
 #pragma unroll
@@ -1058,13 +1180,18 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const float x = bf16f((uint16_t)(w[e >> 1] >> (16 * (e & 1))));
-                const float qv = fminf(fmaxf(rintf(__fmul_rn(x, r)), -fq), fq);
-                o[e >> 2] |= ((uint32_t)(int)qv & 0xFFu) << (8 * (e & 3));
+                const int qv = (int)fminf(fmaxf(rintf(__fmul_rn(x, r)), -fq), fq);
+                if (i0 + 32 * u < n8) qsum += qv;
+                o[e >> 2] |= (e4 ? code_byte<true>(qv) : code_byte<false>(qv)) << (8 * (e & 3));
               }
               if (i0 + 32 * u < n8) dst[i0 + 32 * u] = make_uint2(o[0], o[1]);
             }
           }
-          if (lane == 0) p.Hs[row] = sc;  // per-token: group 0 of the group-major [g][R] layout
+          if (e4) qsum = warp_sum(qsum);
+          if (lane == 0) {
+            p.Hs[row] = sc;  // per-token: group 0 of the group-major [g][R] layout
+            if (e4) p.Hc[row] = qsum;
+          }
         }
         named_bar_sync(1, 256);
         if (ew == 0 && lane == 0) {
@@ -1085,6 +1212,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
       float* cw_sa = ctl.cw[ew][0];
       float* cw_rw = ctl.cw[ew][1];
+      float* cw_sb = ctl.cw[ew][2];
       const int cl = col0 + lane, ch = col0 + 32 + lane;
       const bool vlo = lane < half && cl < t.rows, vhi = 32 + lane < half && ch < t.rows;
       if (t.phase == 2) {  // route weights of this warp's columns, read back as broadcast float4s
@@ -1094,7 +1222,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         __syncwarp();
       }
       const LinDesc& Ld = E.blk[2];
-      const int dmode = !kind_is_i8(Ld.geo.kind) ? 0 : (Ld.geo.group == 128 ? 2 : 1);
+      const int dmode = !kind_is_wa(Ld.geo.kind) ? 0 : (Ld.geo.group == 128 ? (kind_is_f8(Ld.geo.kind) ? 3 : 2) : 1);
       const int dqmax = (1 << (Ld.a_bits - 1)) - 1;
       if (!reg_mode) {
         // ======== streaming epilogue: one drain event for the whole task (dual phase 0, or phase 2)
@@ -1103,7 +1231,9 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         const int slice = task_slice(t);
         const bool two = s.nmats == 2;
         const float* xs_s = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;  // group-major [g][R]
+        const int32_t* xc_s = (t.phase == 0) ? p.xc[s.mat[0]->in_slot] : p.Hc;
         float sw0 = 1.f, sw1 = 1.f, sa_lo = 1.f, sa_hi = 1.f;
+        int qs_lo = 0, qs_hi = 0;
         if (s.i8 && t.phase == 0) {  // x-scales / weight scales exist before this kernel: load before the wait
           const uint16_t* wsc0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off);
           const uint16_t* wsc1 = reinterpret_cast<const uint16_t*>(s.mat[s.nmats - 1]->packed +
@@ -1112,6 +1242,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           sw1 = bf16f(__ldg(wsc1 + n1));
           sa_lo = vlo ? __ldg(xs_s + (int64_t)t.row0 + cl) : 0.f;
           sa_hi = vhi ? __ldg(xs_s + (int64_t)t.row0 + ch) : 0.f;
+          if (s.f8) {
+            qs_lo = vlo ? __ldg(xc_s + (int64_t)t.row0 + cl) : 0;
+            qs_hi = vhi ? __ldg(xc_s + (int64_t)t.row0 + ch) : 0;
+          }
         }
         const uint32_t b0 = abuf;
         abuf = (abuf + 1) & (kAccBufs - 1);
@@ -1125,20 +1259,39 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           sw1 = bf16f(__ldg(wsc0 + n1));
           sa_lo = vlo ? __ldcg(xs_s + (int64_t)t.row0 + cl) : 0.f;
           sa_hi = vhi ? __ldcg(xs_s + (int64_t)t.row0 + ch) : 0.f;
+          if (s.f8) {
+            qs_lo = vlo ? __ldcg(xc_s + (int64_t)t.row0 + cl) : 0;
+            qs_hi = vhi ? __ldcg(xc_s + (int64_t)t.row0 + ch) : 0;
+          }
         }
         if (s.i8) {
           __syncwarp();
-          cw_sa[lane] = sa_lo;
-          cw_sa[32 + lane] = sa_hi;
+          if (s.f8) {  // w4a4: acc * (s_a 2^18) - 8 s_a sum(q_a); the correction once per K (slice 0 of a split)
+            const bool corr = !split || slice == 0;
+            cw_sa[lane] = sa_lo * 262144.f;
+            cw_sa[32 + lane] = sa_hi * 262144.f;
+            cw_sb[lane] = corr ? __fmul_rn(-8.f * (float)qs_lo, sa_lo) : 0.f;
+            cw_sb[32 + lane] = corr ? __fmul_rn(-8.f * (float)qs_hi, sa_hi) : 0.f;
+          } else {
+            cw_sa[lane] = sa_lo;
+            cw_sa[32 + lane] = sa_hi;
+          }
           __syncwarp();
         }
         const uint32_t colA = b0 * (uint32_t)kAccCols;
         const uint32_t colB = colA + (uint32_t)kMat1Col;
+        if constexpr (DUMP) {
+          if (s.i8)
+            dump_event(p, lane_addr + colA + (uint32_t)col0, lane_addr + colB + (uint32_t)col0, two,
+                       t.phase == 0 ? 0 : 2, t.phase == 0 ? 1 : 2, 0, n, t.phase == 0 ? n : n1,
+                       (int64_t)t.row0 + col0, half, nvalid);
+        }
         const float2 swa = make_float2(sw0, sw0), swb = make_float2(sw1, sw1);
 #ifndef MXM_ABL_EPI
         // specialised on (W-A, two mats, phase 0): with run-time flags the compiler predicates both variants
-        auto stream = [&](auto i8_c, auto two_c, auto p0_c) {
+        auto stream = [&](auto i8_c, auto two_c, auto p0_c, auto f8_c) {
         constexpr bool I8 = decltype(i8_c)::value, TWO = decltype(two_c)::value, P0 = decltype(p0_c)::value;
+        constexpr bool F8 = decltype(f8_c)::value;
 #pragma unroll 1
         for (int c = 0; c < half; c += 8) {
           uint32_t va[8], vb[8];
@@ -1152,7 +1305,25 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             fa[j] = __uint_as_float(va[j]);
             fb[j] = TWO ? __uint_as_float(vb[j]) : 0.f;
           }
-          if constexpr (I8) {  // per-column activation scale: broadcast smem reads
+          if constexpr (I8 && F8) {  // w4a4: s_w * (acc * a + b) per column (a, b broadcast from smem)
+            const float4 x0 = *reinterpret_cast<const float4*>(cw_sa + c);
+            const float4 x1 = *reinterpret_cast<const float4*>(cw_sa + c + 4);
+            const float4 y0 = *reinterpret_cast<const float4*>(cw_sb + c);
+            const float4 y1 = *reinterpret_cast<const float4*>(cw_sb + c + 4);
+            const float2 a2s[4] = {make_float2(x0.x, x0.y), make_float2(x0.z, x0.w), make_float2(x1.x, x1.y),
+                                   make_float2(x1.z, x1.w)};
+            const float2 b2s[4] = {make_float2(y0.x, y0.y), make_float2(y0.z, y0.w), make_float2(y1.x, y1.y),
+                                   make_float2(y1.z, y1.w)};
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+              const float2 a2 = fmul2(ffma2(make_float2(fa[j], fa[j + 1]), a2s[j / 2], b2s[j / 2]), swa);
+              fa[j] = a2.x; fa[j + 1] = a2.y;
+              if constexpr (TWO) {
+                const float2 b2 = fmul2(ffma2(make_float2(fb[j], fb[j + 1]), a2s[j / 2], b2s[j / 2]), swb);
+                fb[j] = b2.x; fb[j + 1] = b2.y;
+              }
+            }
+          } else if constexpr (I8) {  // per-column activation scale: broadcast smem reads
             const float4 x0 = *reinterpret_cast<const float4*>(cw_sa + c);
             const float4 x1 = *reinterpret_cast<const float4*>(cw_sa + c + 4);
             const float2 s2[4] = {make_float2(x0.x, x0.y), make_float2(x0.z, x0.w), make_float2(x1.x, x1.y),
@@ -1177,7 +1348,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             uint16_t hb[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) hb[j] = f2bf(silu_f(fa[j]) * fb[j]);
-            emit_h8(p, t, dmode, dqmax, n, col0 + c, nvalid - c, hb, ctl, wg, q, lane, rbuf);
+            emit_h8<DUMP>(p, t, dmode, dqmax, n, col0 + c, nvalid - c, hb, ctl, wg, q, lane, rbuf);
           } else if (split) {  // split-K slice: fp32 partial sums (reduced below by the last slice)
             float* q0 = p.P + ((int64_t)slice * kSplitRows + t.row0 + col0 + c) * p.d + n;
             float* q1 = p.P + ((int64_t)slice * kSplitRows + t.row0 + col0 + c) * p.d + n1;
@@ -1207,11 +1378,13 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         using Tt = std::true_type;
         using Ft = std::false_type;
         if (t.phase == 0) {
-          if (s.i8) { if (two) stream(Tt{}, Tt{}, Tt{}); else stream(Tt{}, Ft{}, Tt{}); }
-          else { if (two) stream(Ft{}, Tt{}, Tt{}); else stream(Ft{}, Ft{}, Tt{}); }
+          if (s.f8) { if (two) stream(Tt{}, Tt{}, Tt{}, Tt{}); else stream(Tt{}, Ft{}, Tt{}, Tt{}); }
+          else if (s.i8) { if (two) stream(Tt{}, Tt{}, Tt{}, Ft{}); else stream(Tt{}, Ft{}, Tt{}, Ft{}); }
+          else { if (two) stream(Ft{}, Tt{}, Tt{}, Ft{}); else stream(Ft{}, Ft{}, Tt{}, Ft{}); }
         } else {
-          if (s.i8) { if (two) stream(Tt{}, Tt{}, Ft{}); else stream(Tt{}, Ft{}, Ft{}); }
-          else { if (two) stream(Ft{}, Tt{}, Ft{}); else stream(Ft{}, Ft{}, Ft{}); }
+          if (s.f8) { if (two) stream(Tt{}, Tt{}, Ft{}, Tt{}); else stream(Tt{}, Ft{}, Ft{}, Tt{}); }
+          else if (s.i8) { if (two) stream(Tt{}, Tt{}, Ft{}, Ft{}); else stream(Tt{}, Ft{}, Ft{}, Ft{}); }
+          else { if (two) stream(Ft{}, Tt{}, Ft{}, Ft{}); else stream(Ft{}, Ft{}, Ft{}, Ft{}); }
         }
 #endif
         tc_fence_before();
@@ -1261,18 +1434,24 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               two ? reinterpret_cast<const uint16_t*>(s.mat[1]->packed + s.mat[1]->geo.wa_scale_off) : wsc0;
           const float* xs_lo = xs_s + (int64_t)t.row0 + cl;
           const float* xs_hi = xs_s + (int64_t)t.row0 + ch;
+          const int32_t* xc_s = (t.phase == 0) ? p.xc[s.mat[0]->in_slot] : p.Hc;
           const int64_t gs = p.hs_stride;
           // g128: per-event scales come through the scale ring. Per-channel: phase 0 reads scales written
           // before this kernel (read-only path, before the wait); phase 2 reads h-scales written by this
           // kernel after the accumulator wait, through L2 (ld.cg)
           const bool pre = t.phase == 0;
           float nsw0 = 1.f, nsw1 = 1.f, nsa_lo = 1.f, nsa_hi = 1.f;
+          int nqs_lo = 0, nqs_hi = 0;
           if (s.i8 && !s.g128) {  // per-channel (one event): scales from global memory
             if (pre) {
               nsw0 = bf16f(__ldg(wsc0 + n));
               if (two) nsw1 = bf16f(__ldg(wsc1 + n1));
               nsa_lo = vlo ? __ldg(xs_lo) : 0.f;
               nsa_hi = vhi ? __ldg(xs_hi) : 0.f;
+              if (s.f8) {
+                nqs_lo = vlo ? __ldg(xc_s + (int64_t)t.row0 + cl) : 0;
+                nqs_hi = vhi ? __ldg(xc_s + (int64_t)t.row0 + ch) : 0;
+              }
             }
           }
           for (int ev = 0; ev < nev; ++ev) {
@@ -1295,8 +1474,18 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               // restage this warp's column scales 16-byte aligned (drain reads them as broadcast float4s)
               const float* src = reinterpret_cast<const float*>(slotp + 512) + aoff + col0;
               __syncwarp();
-              cw_sa[lane] = lane < half ? src[lane] : 0.f;
-              if (half > 32) cw_sa[32 + lane] = 32 + lane < half ? src[32 + lane] : 0.f;
+              if (s.f8) {  // w4a4: a = s_a 2^18, b = -8 s_a sum(q_a) of the group (drain_event F8)
+                const int32_t* qsrc = reinterpret_cast<const int32_t*>(slotp + 1024) + aoff + col0;
+                cw_sa[lane] = lane < half ? src[lane] * 262144.f : 0.f;
+                cw_sb[lane] = lane < half ? __fmul_rn(-8.f * (float)qsrc[lane], src[lane]) : 0.f;
+                if (half > 32) {
+                  cw_sa[32 + lane] = 32 + lane < half ? src[32 + lane] * 262144.f : 0.f;
+                  cw_sb[32 + lane] = 32 + lane < half ? __fmul_rn(-8.f * (float)qsrc[32 + lane], src[32 + lane]) : 0.f;
+                }
+              } else {
+                cw_sa[lane] = lane < half ? src[lane] : 0.f;
+                if (half > 32) cw_sa[32 + lane] = 32 + lane < half ? src[32 + lane] : 0.f;
+              }
               __syncwarp();
               sa_ev = cw_sa;
             } else if (s.i8) {
@@ -1305,22 +1494,41 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
                 if (two) sw1 = bf16f(__ldg(wsc1 + n1));
                 nsa_lo = vlo ? __ldcg(xs_lo) : 0.f;
                 nsa_hi = vhi ? __ldcg(xs_hi) : 0.f;
+                if (s.f8) {
+                  nqs_lo = vlo ? __ldcg(xc_s + (int64_t)t.row0 + cl) : 0;
+                  nqs_hi = vhi ? __ldcg(xc_s + (int64_t)t.row0 + ch) : 0;
+                }
               }
               __syncwarp();
-              cw_sa[lane] = nsa_lo;
-              cw_sa[32 + lane] = nsa_hi;
+              if (s.f8) {
+                cw_sa[lane] = nsa_lo * 262144.f;
+                cw_sa[32 + lane] = nsa_hi * 262144.f;
+                cw_sb[lane] = __fmul_rn(-8.f * (float)nqs_lo, nsa_lo);
+                cw_sb[32 + lane] = __fmul_rn(-8.f * (float)nqs_hi, nsa_hi);
+              } else {
+                cw_sa[lane] = nsa_lo;
+                cw_sa[32 + lane] = nsa_hi;
+              }
               __syncwarp();
             }
             const uint32_t colA = b0 * (uint32_t)kAccCols;
             const uint32_t colB = colA + (uint32_t)kMat1Col;
             const bool dst_hi = t.phase == 0 && nsl == 2 && si == 1;  // hetero: the up sub-loop
             const uint32_t aA = lane_addr + colA + (uint32_t)col0, aB = lane_addr + colB + (uint32_t)col0;
+            if constexpr (DUMP) {
+              if (s.i8) {
+                const int jA = t.phase != 0 ? 2 : (nsl == 2 ? si : 0);
+                const int jB = t.phase != 0 ? 2 : 1;
+                dump_event(p, aA, aB, two, jA, jB, s.g128 ? ev : 0, n, t.phase == 0 ? n : n1,
+                           (int64_t)t.row0 + col0, half, nvalid);
+              }
+            }
 #ifndef MXM_ABL_EPI
             const unsigned long long t_dr = prof_on ? clock64() : 0ull;
             if (dst_hi)
-              drain_event_any<16>(half, acc2, aA, aB, s.i8, false, s.g128, sw0, sw1, sa_ev);
+              drain_event_any<16>(half, acc2, aA, aB, s.i8, s.f8, false, s.g128, sw0, sw1, sa_ev);
             else
-              drain_event_any<0>(half, acc2, aA, aB, s.i8, two, s.g128, sw0, sw1, sa_ev);
+              drain_event_any<0>(half, acc2, aA, aB, s.i8, s.f8, two, s.g128, sw0, sw1, sa_ev);
             if (prof_on) pc[12] += clock64() - t_dr;  // register-accumulating drain time (diagnostic build)
 #endif
             tc_fence_before();
@@ -1340,7 +1548,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               uint16_t hb[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) hb[j] = f2bf(silu_f(acc[cc * 8 + j]) * acc[32 + cc * 8 + j]);
-              emit_h8(p, t, dmode, dqmax, n, col0 + cc * 8, nvalid - cc * 8, hb, ctl, wg, q, lane, rbuf);
+              emit_h8<DUMP>(p, t, dmode, dqmax, n, col0 + cc * 8, nvalid - cc * 8, hb, ctl, wg, q, lane, rbuf);
             }
           }
         } else {
@@ -1402,18 +1610,31 @@ cudaError_t debug_nan_info(unsigned long long* out, bool reset) {
 }
 #endif
 cudaError_t launch_moe_gemm(const GemmParams& prm, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(moe_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(moe_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
+  // the dynamic-smem opt-in is per device: remember it per device ordinal (first use on each GPU)
+  static std::mutex mu;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr_set[dev]) {
+      e = cudaFuncSetAttribute(moe_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(moe_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(moe_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      if (e != cudaSuccess) return e;
+      attr_set[dev] = true;
+    }
   }
-  if (prm.P != nullptr)
-    moe_gemm_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(prm);
+  if (prm.dump != nullptr)
+    moe_gemm_kernel<false, true><<<grid, kThreads, kSmemBytes, st>>>(prm);
+  else if (prm.P != nullptr)
+    moe_gemm_kernel<true, false><<<grid, kThreads, kSmemBytes, st>>>(prm);
   else
-    moe_gemm_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(prm);
+    moe_gemm_kernel<false, false><<<grid, kThreads, kSmemBytes, st>>>(prm);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,8 @@ struct GemmParams {
   const int32_t* grp_n1;
   const int32_t* grp_nq;
   const float* xs[3];  // activation scales of the gate/up input slots (index 1, 2), group-major [g][R]
+  const int32_t* xc[3];  // code sums of the gate/up input slots (index 1, 2), group-major [g][R] (w4a4 correction)
+  int32_t* Hc;           // code sums of h, group-major [g][R]
   uint16_t* H;
   int8_t* Hq;
   float* Hs;           // h scales, group-major [g][R]
@@ -29,6 +31,9 @@ struct GemmParams {
   int32_t* red_cnt;  // split-K arrival counters [group][d/128]
   int d, f_max;
   unsigned long long* prof;  // optional [grid][16] cycle counters per wait site (nullptr = off)
+  // test-only accumulator dump (mxm_debug_moe_group_gemm_dump; nullptr in the product launch): the raw 32-bit
+  // accumulator of every weight-activation drain event (layout: gemm.cu dump_index)
+  uint32_t* dump;
 };
 
 cudaError_t launch_quantize(const PackGeom& g, const void* w, void* codes, void* scale, void* zero, int32_t* err,
@@ -46,7 +51,8 @@ cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T
                               void* scratch, cudaStream_t st);
 cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, const int32_t* row_exp,
                                 const int32_t* v_off, int V, const ExpertDesc* ex, int64_t R, void* Xb, void* XqA,
-                                float* XsA, void* XqB, float* XsB, uint32_t* hmax, cudaStream_t st);
+                                float* XsA, void* XqB, float* XsB, int32_t* XcA, int32_t* XcB, uint32_t* hmax,
+                                cudaStream_t st);
 cudaError_t launch_combine(const void* O, int d, int64_t T, int k, int S, const int32_t* inv, void* y,
                            cudaStream_t st);
 cudaError_t launch_plan(const ExpertDesc* ex, int V, int E, int64_t T, int d, const int32_t* v_off, int g_max,

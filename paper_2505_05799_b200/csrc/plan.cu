@@ -55,10 +55,10 @@ __device__ __forceinline__ int pow2_tile(int m) {
 
 __device__ __forceinline__ float tile_cost(const ExpertDesc& e, int d, int nt) {
   const LinDesc& g = e.blk[0];
-  const float rate = kind_is_i8(g.geo.kind) ? 8192.f : 4096.f;  // MAC / cycle / SM
+  const float rate = kind_is_wa(g.geo.kind) ? 8192.f : 4096.f;  // MAC / cycle / SM
   const float mma = 2.f * 128.f * (float)nt * (float)d / rate;
   const float wbytes = 2.f * 128.f * (float)d * (float)g.geo.w_bits / 8.f;
-  const float bbytes = (float)nt * (float)d * (kind_is_i8(g.geo.kind) ? 1.f : 2.f);
+  const float bbytes = (float)nt * (float)d * (kind_is_wa(g.geo.kind) ? 1.f : 2.f);
   const float mem = (wbytes + bbytes) / 24.f;
   return fmaxf(mma, mem) + 400.f;
 }
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
     const int v = tid;
     const ExpertDesc& e = ex[v];
     // h-quant pass only for per-token W-A downs (g128 downs are quantized in the gate/up epilogue)
-    const bool wa_down = kind_is_i8(e.blk[2].geo.kind) && e.blk[2].geo.group != 128;
+    const bool wa_down = kind_is_wa(e.blk[2].geo.kind) && e.blk[2].geo.group != 128;
     for (int i = 0; i < s_nfull[v]; ++i) {
       const int g = s_base[v] + i;
       grp_v[g] = v;

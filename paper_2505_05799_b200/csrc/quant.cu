@@ -1,5 +1,5 @@
 // quant.cu — setup kernels: weight quantizer (S0a), packer (S0b), debug dequantizer,
-// and the standalone activation quantizer entry (the same device function the hot path uses).
+// and the standalone activation quantizer entry (quant_row_warp, the hot path's gate/up input quantizer).
 //
 // Weight quantizer Q (§2.1; 16-bit meta P:339; groups along K P:452), readings
 // DESIGN.md R1-R7: fp64 arithmetic, stored scale = smallest bf16 s with c*s >= range, codes
@@ -109,7 +109,7 @@ __global__ void pack_kernel(PackGeom g, const uint8_t* __restrict__ codes, const
       *reinterpret_cast<uint4*>(chunk + r * 128 + ((c ^ (r & 7)) << 4)) = v;
     }
   } else {
-    const bool i8k = g.kind == KIND_WA_ROW;
+    const bool i8k = kind_is_row8(g.kind);
     uint8_t* p = chunk;
     if (chunk_has_meta(g, ks)) {
       const int64_t gi = k0 / g.group, ng = g.K / g.group;
@@ -138,7 +138,7 @@ __global__ void pack_kernel(PackGeom g, const uint8_t* __restrict__ codes, const
       shift += pb;
     }
   }
-  if (kind_is_i8(g.kind) && ks == 0) {
+  if (kind_is_wa(g.kind) && ks == 0) {
     const int64_t ng = g.K / g.group;
     uint16_t* sc = reinterpret_cast<uint16_t*>(out + g.wa_scale_off);
     for (int64_t gi = 0; gi < ng; ++gi) sc[gi * g.N + n] = scale[n * ng + gi];
@@ -153,7 +153,7 @@ __device__ uint32_t read_stored_code(const PackGeom& g, const uint8_t* packed, i
     const int b = i;
     return chunk[r * 128 + (((b >> 4) ^ (r & 7)) << 4) + (b & 15)];
   }
-  const bool i8k = g.kind == KIND_WA_ROW;
+  const bool i8k = kind_is_row8(g.kind);
   const uint8_t* p = chunk + (chunk_has_meta(g, ks) ? g.meta_bytes : 0);
   const int planes[2] = {g.w_bits == 3 ? 2 : (g.w_bits == 5 ? 4 : g.w_bits), (g.w_bits == 3 || g.w_bits == 5) ? 1 : 0};
   uint32_t u = 0;
@@ -186,7 +186,7 @@ __global__ void dequant_kernel(PackGeom g, const uint8_t* __restrict__ packed, f
   const int gi = (int)(k / g.group);
   double s, z = 0;
   int q;
-  if (kind_is_i8(g.kind)) {
+  if (kind_is_wa(g.kind)) {
     q = g.kind == KIND_WA_IMG ? (int)(int8_t)u : (int)u - (1 << (g.w_bits - 1));
     s = bf16_bits_to_double(reinterpret_cast<const uint16_t*>(packed + g.wa_scale_off)[(int64_t)gi * g.N + n]);
   } else {
@@ -200,19 +200,27 @@ __global__ void dequant_kernel(PackGeom g, const uint8_t* __restrict__ packed, f
 }
 
 // ---------------------------------------------------------------- activation quantizer (debug entry)
-// one warp per (row, group)
+// One warp per row, through the hot path's gate/up input quantizer (quant_row_warp, actq.cuh; route.cu gather)
+// with canonical two's complement codes; rows longer than 4096 use its per-group fallback (quant_group_warp).
+// The gather writes group-major [g][R] scales; here row-major [M][K/g] (stride 1 between groups of a row).
 __global__ void act_quant_kernel(const uint16_t* __restrict__ v, int64_t M, int64_t K, int a_bits, int group,
                                  int8_t* __restrict__ codes, float* __restrict__ scale, int32_t* __restrict__ qsum) {
   const int64_t ng = K / group;
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  if (w >= M * ng) return;
-  const int64_t m = w / ng, gi = w % ng;
-  int qs;
-  const float s = quant_group_warp(v + m * K + gi * group, codes + m * K + gi * group, group,
-                                   (1 << (a_bits - 1)) - 1, &qs);
-  if ((threadIdx.x & 31) == 0) {
-    scale[m * ng + gi] = s;
-    if (qsum) qsum[m * ng + gi] = qs;
+  const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (m >= M) return;
+  const int qmax = (1 << (a_bits - 1)) - 1;
+  if (K <= 128 * 32) {
+    quant_row_warp<32, false>(v + m * K, codes + m * K, (int)K, group, qmax, scale + m * ng,
+                              qsum ? qsum + m * ng : nullptr, 1);
+    return;
+  }
+  for (int64_t gi = 0; gi < ng; ++gi) {
+    int qs;
+    const float s = quant_group_warp<false, false>(v + m * K + gi * group, codes + m * K + gi * group, group, qmax, &qs);
+    if ((threadIdx.x & 31) == 0) {
+      scale[m * ng + gi] = s;
+      if (qsum) qsum[m * ng + gi] = qs;
+    }
   }
 }
 
@@ -238,7 +246,7 @@ cudaError_t launch_dequantize(const PackGeom& g, const void* packed, float* out,
 }
 cudaError_t launch_act_quant(const void* v, int64_t M, int64_t K, int a_bits, int group, void* codes, float* scale,
                              int32_t* qsum, cudaStream_t st) {
-  const int64_t warps = M * (K / group);
+  const int64_t warps = M;
   act_quant_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
       (const uint16_t*)v, M, K, a_bits, group, (int8_t*)codes, scale, qsum);
   return cudaGetLastError();

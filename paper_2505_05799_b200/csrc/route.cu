@@ -167,7 +167,8 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
                                     const int32_t* __restrict__ row_exp, const int32_t* __restrict__ v_off, int V,
                                     const ExpertDesc* __restrict__ ex,
                                     int64_t R, uint16_t* __restrict__ Xb, int8_t* __restrict__ XqA, float* __restrict__ XsA,
-                                    int8_t* __restrict__ XqB, float* __restrict__ XsB, uint32_t* __restrict__ hmax) {
+                                    int8_t* __restrict__ XqB, float* __restrict__ XsB, int32_t* __restrict__ XcA,
+                                    int32_t* __restrict__ XcB, uint32_t* __restrict__ hmax) {
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (row >= R) return;
@@ -187,14 +188,24 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
     } else if constexpr (QUANT) {
       int8_t* q = (L.in_slot == 1 ? XqA : XqB) + row * d;
       float* sc = (L.in_slot == 1 ? XsA : XsB) + row;  // group-major [g][R]
+      int32_t* qs = (L.in_slot == 1 ? XcA : XcB) + row;
       const int g = L.a_group == -1 ? d : L.a_group;
       const int qmax = (1 << (L.a_bits - 1)) - 1;
-      if (d <= 128 * 32 && (g == 128 || g == d)) {
-        quant_row_warp<32>(src, q, d, g, qmax, sc, R);  // whole row in registers, all loads in flight
+      const bool e4 = kind_is_f8(L.geo.kind);  // w4a4: e4m3 codes for kind::f8f6f4 (common.cuh)
+      if (d <= 128 * 32 && (g == 128 || g == d)) {  // whole row in registers, all loads in flight
+        if (e4)
+          quant_row_warp<32, true>(src, q, d, g, qmax, sc, qs, R);
+        else
+          quant_row_warp<32, false>(src, q, d, g, qmax, sc, qs, R);
       } else {
         for (int gi = 0; gi < d / g; ++gi) {
-          const float s = quant_group_warp(src + gi * g, q + gi * g, g, qmax, nullptr);
-          if (lane == 0) sc[gi * R] = s;
+          int qsum = 0;
+          const float s = e4 ? quant_group_warp<false, true>(src + gi * g, q + gi * g, g, qmax, &qsum)
+                             : quant_group_warp<false, false>(src + gi * g, q + gi * g, g, qmax, &qsum);
+          if (lane == 0) {
+            sc[gi * R] = s;
+            qs[gi * R] = qsum;
+          }
         }
       }
     }
@@ -274,16 +285,16 @@ cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T
 cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, const int32_t* row_exp,
                                 const int32_t* v_off, int V,
                                 const ExpertDesc* ex, int64_t R, void* Xb, void* XqA, float* XsA, void* XqB, float* XsB,
-                                uint32_t* hmax, cudaStream_t st) {
+                                int32_t* XcA, int32_t* XcB, uint32_t* hmax, cudaStream_t st) {
   if (R <= 0) return cudaSuccess;
   if (XqA != nullptr || XqB != nullptr)
     gather_quant_kernel<true><<<(unsigned)((R * 32 + 255) / 256), 256, 0, st>>>(
         (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB,
-        hmax);
+        XcA, XcB, hmax);
   else
     gather_quant_kernel<false><<<(unsigned)((R * 32 + 255) / 256), 256, 0, st>>>(
         (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB,
-        hmax);
+        XcA, XcB, hmax);
   return cudaGetLastError();
 }
 

@@ -129,6 +129,25 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// kind::f8f6f4 (e4m3 x e4m3 inputs, f32 accum): the w4a4 path (common.cuh KIND_WA_F8)
+__device__ __forceinline__ void mma_f8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // A operand from TMEM (TS form): D[tmem] (+)= A[tmem] * B[smem]^T. A row r = TMEM lane r.
 __device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
@@ -223,6 +242,10 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t n) {
          | (1u << 7)        // a_format BF16
          | (1u << 10)       // b_format BF16
          | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
+// kind::f8f6f4, A and B e4m3 (format 0), f32 accumulator
+__host__ __device__ constexpr uint32_t idesc_f8(uint32_t n) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
 __host__ __device__ constexpr uint32_t idesc_s8(uint32_t n, bool a_signed = true, bool b_signed = true) {
   return (2u << 4)  // c_format S32

@@ -1,10 +1,6 @@
 #!/bin/bash
-# run the GPU test suites with hard timeouts; logs land in gpurun_out/
+# GPU parity suite (+ optional extra pytest args) -> gpurun_out/pytest_gpu.log
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
-for f in "$@"; do
-  b=$(basename $f .py)
-  timeout ${TEST_TIMEOUT:-600} python -m pytest $f -x -q -m gpu -p no:cacheprovider > gpurun_out/$b.log 2>&1
-  echo "$f rc=$?" >> gpurun_out/summary.txt
-  tail -15 gpurun_out/$b.log
-done
+timeout ${PYTEST_TIMEOUT:-1500} python -m pytest tests -q -m gpu -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -30 gpurun_out/pytest_gpu.log
