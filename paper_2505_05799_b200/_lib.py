@@ -82,11 +82,13 @@ def load(path: str = LIB_PATH):
     if _lib is not None:
         return _lib
     # experiment variants built in-tree by build.build_variant (tools/); default: the product library
-    path = os.environ.get("MXM_LIB", path)
+    path = os.environ.get("MXM_LIB") or path
     if not os.path.exists(path):
         raise MxmError(MXM_E_CUDA, f"{path} not built; run __graft_entry__.build() (no CPU fallback exists)")
     lib = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
+        if path != LIB_PATH and not hasattr(lib, name):
+            continue  # an older experiment variant (tools/variants) may lack newer debug entries
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -29,7 +29,16 @@
 
 namespace mxm {
 
-constexpr int kStages = 4;
+#ifndef MXM_STAGES
+#define MXM_STAGES 4
+#endif
+#ifndef MXM_TILE_KB
+#define MXM_TILE_KB 16
+#endif
+#ifndef MXM_SSLOTS
+#define MXM_SSLOTS 4
+#endif
+constexpr int kStages = MXM_STAGES;
 constexpr int kRing = 4;
 // TMEM (512 columns): two accumulator buffers of 192 columns at [0, 384) -- a dual tile (gate | up, or two
 // 128-channel down tiles) of up to 96 tokens fits one buffer, so every task is double-buffered against the
@@ -44,9 +53,9 @@ constexpr int kMat1Col = kAccCols / 2;               // column offset of mat 1 i
 constexpr int kTmemA = kAccBufs * kAccCols;
 static_assert(kTmemA + 64 * kASlots == 512, "TMEM partition");
 static_assert(kMat1Col == MXM_DUAL_TILE, "dual token tile (common.cuh) must match the accumulator buffer");
-constexpr int kThreads = 640;  // 20 warps: producer, MMA issuer, 2 idle, 4 transform, 8 epilogue, 4 transform
+constexpr int kThreads = 640;  // 20 warps: producer, MMA issuer, 2 scale staging, 4 transform, 8 epilogue, 4 transform
 constexpr int kXfWarps = 8;     // transform warps 4..7 (K half 0) and 16..19 (K half 1); one A row per thread
-constexpr int kTileBytes = 16384;
+constexpr int kTileBytes = MXM_TILE_KB * 1024;
 constexpr int kSlotBytes = 3 * kTileBytes;  // per stage: token tile B | mat 0 (raw codes or A image) | mat 1
 
 constexpr int kOffCtl = kStages * kSlotBytes;
@@ -55,16 +64,21 @@ constexpr int kCtlBytes = 8192;
 // weight scales (128 bf16 per mat) and activation scales (the m-tile's rows of the group-major [g][R]
 // array, from the 16-byte-aligned floor) next to the stage's operands; the epilogue drains the event's
 // accumulator against them, then releases the slot.
-constexpr int kSSlots = 4;
-// [0,256) mat-0 s_w | [256,512) mat-1 s_w | [512,1024) s_a (<= 125 floats) | [1024,1536) code sums (w4a4)
-constexpr int kSSlotBytes = 1536;
+constexpr int kSSlots = MXM_SSLOTS;
+// [0,256) mat-0 s_w | [256,512) mat-1 s_w | [512,1024) s_a (<= 125 floats) | [1024,1536) code sums (w4a4),
+// all as bulk-copied (s_a / sums from the 16-B aligned floor of the m-tile's span) | [1536,2048) per token column
+// drain factor a (s_a, or s_a 2^18 for w4a4) | [2048,2560) w4a4 offset correction b = -8 s_a sum(q_a): written,
+// 16-B aligned from column 0, once the bulk copies landed, by the scale-staging warps (sready), so the epilogue reads
+// them as broadcast float4s with no per-warp restaging on its critical path (scale-staging warps 2-3)
+constexpr int kSSlotBytes = 2560;
+constexpr int kSlotA = 1536, kSlotB = 2048;
 constexpr int kOffScale = kOffCtl + kCtlBytes;
 constexpr int kSmemBytes = kOffScale + kSSlots * kSSlotBytes + 1024;
 
 struct Ctl {
   uint64_t full[kStages], empty[kStages];
   uint64_t aready[kASlots], aempty[kASlots];
-  uint64_t sfull[kSSlots], sempty[kSSlots];
+  uint64_t sfull[kSSlots], sempty[kSSlots], sready[kSSlots];
   uint64_t accf[kAccBufs], acce[kAccBufs];
   uint64_t tfull[kRing], tempty[kRing];
   Task ring[kRing];
@@ -157,7 +171,7 @@ __device__ __forceinline__ bool bf2_nonfinite(uint32_t v) {
 #ifdef MXM_TRACE
 // per-stage event timestamps of CTA 0 (diagnostic build): [event][index], see tools/diag_trace.py
 constexpr int kTrN = 2048;
-__device__ unsigned long long g_tr[8][kTrN];
+__device__ unsigned long long g_tr[12][kTrN];
 #define TR(ev, idx) do { if (blockIdx.x == 0 && (idx) < kTrN) g_tr[ev][idx] = clock64(); } while (0)
 #else
 #define TR(ev, idx) do { } while (0)
@@ -414,6 +428,40 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
   constexpr int CH = 8;  // 16-wide staging + 64 accumulators exceeds the 128-register epilogue budget (spills)
   constexpr int NCH = HALF / CH;
   constexpr float kMagic = 12582912.f;  // 2^23 + 2^22
+  if constexpr (I8 && F8) {
+    // per 8-column chunk: both mats' TMEM loads and the chunk's factors (a, b: broadcast float4s) in flight
+    // together, one wait, then 2 FFMA2 per element pair (no cross-chunk software pipelining: at 128
+    // registers ptxas serialises it anyway, and one round trip per chunk is what that costs)
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int c0 = c * CH;
+      uint32_t xa[CH], xb[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) xb[j] = 0u;
+      tmem_ld8(addrA + c0, xa);
+      if constexpr (TWO) tmem_ld8(addrB + c0, xb);
+      const float4 a0 = *reinterpret_cast<const float4*>(sa + c0);
+      const float4 a1 = *reinterpret_cast<const float4*>(sa + c0 + 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(sa + 128 + c0);
+      const float4 b1 = *reinterpret_cast<const float4*>(sa + 128 + c0 + 4);
+      tmem_ld_wait_regs(xa, xb);
+      const float2 ac[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
+                            make_float2(a1.z, a1.w)};
+      const float2 bc[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                            make_float2(b1.z, b1.w)};
+#pragma unroll
+      for (int j = 0; j < CH; j += 2) {
+        const int col = c0 + j;
+        const float2 fa = make_float2(__uint_as_float(xa[j]), __uint_as_float(xa[j + 1]));
+        acc2[DST0 + col / 2] = ffma2(ffma2(fa, ac[j / 2], bc[j / 2]), make_float2(sw0, sw0), acc2[DST0 + col / 2]);
+        if constexpr (TWO) {
+          const float2 fb = make_float2(__uint_as_float(xb[j]), __uint_as_float(xb[j + 1]));
+          acc2[16 + col / 2] = ffma2(ffma2(fb, ac[j / 2], bc[j / 2]), make_float2(sw1, sw1), acc2[16 + col / 2]);
+        }
+      }
+    }
+    return;
+  }
   // software-pipelined: chunk c+1's TMEM loads are in flight while chunk c is scaled and accumulated
   uint32_t va[2][CH], vb[2][CH];
 #pragma unroll
@@ -442,22 +490,7 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
       }
     } else
 #endif
-    if constexpr (I8 && F8) {
-#pragma unroll
-      for (int j = 0; j < CH; j += 2) {
-        const int col = c0 + j;
-        const float4 sa4 = *reinterpret_cast<const float4*>(sa + (col & ~3));  // 16-B aligned, broadcast
-        const float4 sb4 = *reinterpret_cast<const float4*>(sa + 128 + (col & ~3));
-        const float2 sac = (col & 2) ? make_float2(sa4.z, sa4.w) : make_float2(sa4.x, sa4.y);
-        const float2 sbc = (col & 2) ? make_float2(sb4.z, sb4.w) : make_float2(sb4.x, sb4.y);
-        const float2 fa = make_float2(__uint_as_float(va[cur][j]), __uint_as_float(va[cur][j + 1]));
-        acc2[DST0 + col / 2] = ffma2(ffma2(fa, sac, sbc), make_float2(sw0, sw0), acc2[DST0 + col / 2]);
-        if constexpr (TWO) {
-          const float2 fb = make_float2(__uint_as_float(vb[cur][j]), __uint_as_float(vb[cur][j + 1]));
-          acc2[16 + col / 2] = ffma2(ffma2(fb, sac, sbc), make_float2(sw1, sw1), acc2[16 + col / 2]);
-        }
-      }
-    } else if constexpr (I8) {
+    if constexpr (I8) {
 #pragma unroll
       for (int j = 0; j < CH; j += 2) {
         const int col = c0 + j;
@@ -824,6 +857,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(&ctl.sfull[i], 1);
       mbar_init(&ctl.sempty[i], 8);  // the 8 epilogue warps
+      mbar_init(&ctl.sready[i], 2);  // the scale-staging warps 2-3 (drain factors staged)
     }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&ctl.accf[i], 1);
@@ -831,7 +865,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     }
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&ctl.tfull[i], 1);
-      mbar_init(&ctl.tempty[i], 1 + kXfWarps + 8);
+      mbar_init(&ctl.tempty[i], 1 + kXfWarps + 8 + 2);  // producer, transform, epilogue, scale staging
     }
     fence_mbar_init();
   }
@@ -1036,6 +1070,53 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         acc_ph = st.acc_ph;
         aidx = st.aidx;
         ntr_m = st.ntr;
+      }
+    }
+    __syncwarp();
+  } else {
+    // =========================== scale staging (warps 2-3): per 128-K group of a g128 W-A sub-loop, once its
+    // scale slot landed (sfull), write the drain factors of every token column 16-B aligned into the slot
+    // (a = s_a, or s_a 2^18 for w4a4; b = -8 s_a sum(q_a)) and signal the epilogue (sready)
+    uint32_t xsidx = 0;
+    const int c0 = (warp - 2) * 32 + lane;  // this thread's token columns: c0 and c0 + 64
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
+      twait(&ctl.tfull[slot], rphase, pc[7], prof_on);
+      const Task t = ctl.ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl.tempty[slot]);
+      if (t.phase == 255) break;
+      if (t.phase == 1) continue;
+      SubLoop sl[2];
+      const int nsl = build_subloops(t, p.ex, p.d, n_split, sl);
+      for (int si = 0; si < nsl; ++si) {
+        const SubLoop& s = sl[si];
+        if (!s.g128) continue;
+        const float* xs_t = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;
+        for (int ks = 0; ks < s.ns; ++ks) {
+          const uint32_t ss = xsidx & (kSSlots - 1);
+          twait(&ctl.sfull[ss], (xsidx / kSSlots) & 1, pc[8], prof_on);
+          uint8_t* slotp = smem + kOffScale + ss * kSSlotBytes;
+          uint32_t aoff;
+          (void)ascale_span(xs_t, p.hs_stride, ks, t.row0, aoff);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c0 + 64 * h;
+            if (c < (int)t.nt) {
+              const float sav = reinterpret_cast<const float*>(slotp + 512)[aoff + c];
+              float av = sav, bv = 0.f;
+              if (s.f8) {
+                av = sav * 262144.f;
+                bv = __fmul_rn(-8.f * (float)reinterpret_cast<const int32_t*>(slotp + 1024)[aoff + c], sav);
+              }
+              reinterpret_cast<float*>(slotp + kSlotA)[c] = av;
+              reinterpret_cast<float*>(slotp + kSlotB)[c] = bv;
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ctl.sready[ss]);
+          ++xsidx;
+        }
       }
     }
     __syncwarp();
@@ -1459,35 +1540,19 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             const uint32_t b0 = abuf;
             abuf = (abuf + 1) & (kAccBufs - 1);
             twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
+            if (threadIdx.x == 256) TR(5, n_tr_e);
             acc_ph ^= 1u << b0;
             tc_fence_after();
             const float* sa_ev = cw_sa;
             uint32_t ss = 0;
             if (s.g128) {  // g128 event: the group's scales arrived in the scale ring with the stage
               ss = sidx & (kSSlots - 1);
-              twait(&ctl.sfull[ss], (sidx / kSSlots) & 1, pc[10], prof_on);
+              twait(&ctl.sready[ss], (sidx / kSSlots) & 1, pc[10], prof_on);  // factors staged by the transform
+              if (threadIdx.x == 256) TR(7, n_tr_e);
               const uint8_t* slotp = smem + kOffScale + ss * kSSlotBytes;
               sw0 = bf16f(reinterpret_cast<const uint16_t*>(slotp)[l]);
               if (two) sw1 = bf16f(reinterpret_cast<const uint16_t*>(slotp + 256)[l]);
-              uint32_t aoff;
-              (void)ascale_span(xs_s, gs, ev, t.row0, aoff);
-              // restage this warp's column scales 16-byte aligned (drain reads them as broadcast float4s)
-              const float* src = reinterpret_cast<const float*>(slotp + 512) + aoff + col0;
-              __syncwarp();
-              if (s.f8) {  // w4a4: a = s_a 2^18, b = -8 s_a sum(q_a) of the group (drain_event F8)
-                const int32_t* qsrc = reinterpret_cast<const int32_t*>(slotp + 1024) + aoff + col0;
-                cw_sa[lane] = lane < half ? src[lane] * 262144.f : 0.f;
-                cw_sb[lane] = lane < half ? __fmul_rn(-8.f * (float)qsrc[lane], src[lane]) : 0.f;
-                if (half > 32) {
-                  cw_sa[32 + lane] = 32 + lane < half ? src[32 + lane] * 262144.f : 0.f;
-                  cw_sb[32 + lane] = 32 + lane < half ? __fmul_rn(-8.f * (float)qsrc[32 + lane], src[32 + lane]) : 0.f;
-                }
-              } else {
-                cw_sa[lane] = lane < half ? src[lane] : 0.f;
-                if (half > 32) cw_sa[32 + lane] = 32 + lane < half ? src[32 + lane] : 0.f;
-              }
-              __syncwarp();
-              sa_ev = cw_sa;
+              sa_ev = reinterpret_cast<const float*>(slotp + kSlotA) + col0;  // b at sa_ev + (kSlotB - kSlotA) / 4
             } else if (s.i8) {
               if (!pre) {  // h-scales are written by this kernel: read after the MMA consumed Hq (ld.cg)
                 sw0 = bf16f(__ldg(wsc0 + n));
@@ -1524,12 +1589,14 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               }
             }
 #ifndef MXM_ABL_EPI
+            if (threadIdx.x == 256) TR(8, n_tr_e);
             const unsigned long long t_dr = prof_on ? clock64() : 0ull;
             if (dst_hi)
               drain_event_any<16>(half, acc2, aA, aB, s.i8, s.f8, false, s.g128, sw0, sw1, sa_ev);
             else
               drain_event_any<0>(half, acc2, aA, aB, s.i8, s.f8, two, s.g128, sw0, sw1, sa_ev);
             if (prof_on) pc[12] += clock64() - t_dr;  // register-accumulating drain time (diagnostic build)
+            if (threadIdx.x == 256) TR(9, n_tr_e);
 #endif
             tc_fence_before();
             __syncwarp();
@@ -1537,6 +1604,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               mbar_arrive(&ctl.acce[b0]);
               if (s.g128) mbar_arrive(&ctl.sempty[ss]);
             }
+            if (threadIdx.x == 256) TR(6, n_tr_e);
+            ++n_tr_e;
             if (s.g128) ++sidx;
           }
         }

@@ -58,8 +58,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 #endif
   return ok != 0;
 }
+#ifndef MXM_WAIT_BACKOFF
+#define MXM_WAIT_BACKOFF 0  // ns of __nanosleep between failed polls (0 = poll back to back)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+#if MXM_WAIT_BACKOFF > 0
+    __nanosleep(MXM_WAIT_BACKOFF);
+#endif
   }
 }
 

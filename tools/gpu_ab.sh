@@ -1,12 +1,13 @@
 #!/bin/bash
-# A/B timing of library variants: VARIANTS="tools/variants/lib_x.so ..." (empty entry = product lib),
-# TABLES="mixed w16 ...", CFG=dsv2. One bench line per (variant, table) in gpurun_out/ab.txt
-mkdir -p gpurun_out
-CFG=${CFG:-dsv2}
-for v in default ${VARIANTS}; do
-  for tb in ${TABLES:-mixed}; do
-    if [ "$v" = default ]; then unset MXM_LIB; else export MXM_LIB=$(pwd)/$v; fi
-    out=$(timeout 300 python bench.py --config $CFG --table $tb --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline --no-e2e --no-comparators ${EXTRA} 2>gpurun_out/ab_err.txt)
-    echo "$v $tb $(echo "$out" | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print("step_ms=%.4f gemm_ms=%.4f frac=%.3f" % (d["ms_per_step"], d["roofline"]["kernel_ms"], d["roofline"]["frac"]))' 2>&1 | tail -1)" | tee -a gpurun_out/ab.txt
+# A/B GEMM time of library variants: VARIANTS="base wait0" SPECS="q2 w4a4_g128_sym;q2 mixed" bash tools/gpu_ab.sh
+mkdir -p gpurun_out; OUT=gpurun_out/ab${TAG}.txt; : > $OUT
+IFS=';' read -ra SP <<< "${SPECS}"
+for spec in "${SP[@]}"; do
+  set -- $spec
+  for v in ${VARIANTS}; do
+    LIBV=""; [ "$v" != "base" ] && LIBV=$(pwd)/tools/variants/lib_$v.so
+    MXM_LIB=$LIBV timeout 300 python bench.py --config $1 --table ${2:-mixed} ${3:+--tokens $3} --steps ${STEPS:-5} --warmup 2 --no-cpu-baseline --no-e2e --no-comparators > /tmp/b.json 2>/tmp/b.err
+    echo "$spec $v rc=$? $(python -c 'import json; d=json.load(open("/tmp/b.json")); print("gemm_ms=%.4f step_ms=%.4f pe_frac=%.3f" % (d["roofline"]["kernel_ms"], d["ms_per_step"], d["per_expert_roofline"]["frac_of_gemm"]))' 2>&1 | tail -1)" >> $OUT
   done
 done
+cat $OUT

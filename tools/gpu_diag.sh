@@ -1,15 +1,13 @@
 #!/bin/bash
-# diagnostics: mixtral crash isolation + wait-site breakdowns
-mkdir -p gpurun_out
-: > gpurun_out/diag_mx.txt
-for tb in w4a16_g128_asym w8a8_g-1_sym mixed; do
-  for T in 64 512; do
-    timeout 120 python bench.py --config mx --tokens $T --table $tb --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-comparators > /tmp/o.json 2>/tmp/o.err
-    echo "mx $tb T=$T rc=$? $(head -c 300 /tmp/o.json) $(grep -m1 -i error /tmp/o.err)" >> gpurun_out/diag_mx.txt
-  done
+# wait-site breakdowns (diag build; DIAG="cfg table[;cfg table...]") + one ncu --set full capture of the GEMM
+mkdir -p gpurun_out; OUT=gpurun_out/diag${TAG}.txt; : > $OUT
+IFS=';' read -ra SPECS <<< "${DIAG}"
+for spec in "${SPECS[@]}"; do
+  [ -n "$spec" ] && timeout 300 python tools/diag_waits.py $spec >> $OUT 2>&1
 done
-: > gpurun_out/diag_waits.txt
-for a in "dsv2 mixed" "q15 mixed" "q15 w8a8_g-1_sym" "q2 mixed" "q2 w8a8_g-1_sym" "q2 w4a4_g128_sym"; do
-  timeout 300 python tools/diag_waits.py $a >> gpurun_out/diag_waits.txt 2>&1
-done
-cat gpurun_out/diag_mx.txt gpurun_out/diag_waits.txt
+if [ -n "$NCUCFG" ]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:moe_gemm -s 1 -c 1 -o gpurun_out/prof_${NCUCFG}${TAG} -f \
+     python bench.py --config $NCUCFG ${NCUARGS} --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-comparators > /dev/null 2>gpurun_out/ncu${TAG}.err
+  echo "ncu rc=$?" >> $OUT
+fi
+cat $OUT
