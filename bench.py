@@ -7,12 +7,14 @@ mxm_moe_group_gemm call (route-prep, act-quant + gather, plan, persistent group-
 combine) over one batch of T tokens whose inputs are resident in HBM; L2 is flushed
 (256 MB memset) before every timed step, outside the timed region.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config dsv2|q15|mx|q2|tiny] [--tokens T]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config q2|dsv2|q15|mx|tiny] [--tokens T]
   python bench.py --impl reference ...   (the CPU oracle on bounded token samples)
 
-N > 1 (torchrun, one rank per GPU): expert parallelism. Rank r owns routed experts
-[r·E/G, (r+1)·E/G) and its own batch of T tokens (weak scaling: per-GPU tokens and per-GPU expert work
-fixed as N grows); tokens are dispatched to / combined from the expert owners with NCCL all-to-all
+Default workload: the BASELINE.json headline, the Qwen2-57B-A14B layer at T = 16384 tokens (the largest
+single-GPU config; 64 routed + 1 shared expert, W-A mix). N > 1: when not already under torchrun, bench.py
+re-executes itself under `torch.distributed.run --nproc-per-node N` (127.0.0.1); each rank then runs expert
+parallelism: rank r owns routed experts [r·E/G, (r+1)·E/G) and its own batch of T tokens
+(weak scaling), tokens are dispatched to / combined from the expert owners with NCCL all-to-all
 (paper_2505_05799_b200/ep.py). `--replicas` instead runs N independent full replicas.
 """
 from __future__ import annotations
@@ -45,12 +47,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--config", default="dsv2")
+    ap.add_argument("--config", default="q2")
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--table", default="mixed", help="mixed | w16 | <scheme name, e.g. w2a16_g128_asym>")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=512, help="tokens in the cpu_baseline oracle sample")
+    ap.add_argument("--cpu-sample", type=int, default=128, help="tokens of the larger cpu_baseline oracle sample")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent full replicas instead of EP")
     return ap.parse_args()
@@ -126,9 +128,16 @@ UNIFORM_COMPARATORS = {
     "dsv2": ["w16", "w2a16_g128_asym"],      # bf16 and the equal-bits (2.25) uniform scheme
     "q15": ["w16", "w8a8_g-1_sym"],          # bf16 and uniform W8A8
     "mx": ["w16", "w8a8_g-1_sym", "w4a16_g128_asym"],
-    "q2": ["w8a8_g-1_sym"],
+    "q2": ["w8a8_g-1_sym", "w16"],
     "tiny": ["w16"],
 }
+
+
+def lib_sha1() -> str:
+    import hashlib
+    from paper_2505_05799_b200 import _lib
+    with open(os.environ.get("MXM_LIB") or _lib.LIB_PATH, "rb") as f:
+        return hashlib.sha1(f.read()).hexdigest()
 
 
 def time_steps(fn, steps, flush):
@@ -159,19 +168,28 @@ def bf16_grouped_block(cfg, Wt, x, ids, w, sw, steps, flush):
     wr = w.reshape(-1)[order].unsqueeze(1).to(torch.bfloat16)
     xs = x[tok]
 
-    def gemms():
+    wsh = [(torch.cat([Wt[E + s][0], Wt[E + s][1]], 0).t().contiguous(), Wt[E + s][2].t().contiguous())
+           for s in range(S)]  # shared experts: dense [d, 2 f_s] and [f_s, d]
+    fs = cfg.shared_inter
+
+    def routed():
         gu = torch._grouped_mm(xs, wgu, offs=offs)
         h = torch.nn.functional.silu(gu[:, :f]) * gu[:, f:]
         return torch._grouped_mm(h, wd, offs=offs)
 
+    def shared(s):
+        gu = x @ wsh[s][0]
+        return (torch.nn.functional.silu(gu[:, :fs]) * gu[:, fs:]) @ wsh[s][1]
+
+    def gemms():  # every expert GEMM of the block, routed and shared (the same FLOPs as the group-GEMM)
+        o = routed()
+        return o, [shared(s) for s in range(S)]
+
     def block():
-        o = gemms() * wr
-        y = torch.zeros(T, d, dtype=torch.float32, device=x.device).index_add_(0, tok, o.float())
+        o, ys = gemms()
+        y = torch.zeros(T, d, dtype=torch.float32, device=x.device).index_add_(0, tok, (o * wr).float())
         for s in range(S):
-            g = x @ Wt[E + s][0].t()
-            u = x @ Wt[E + s][1].t()
-            ys = (torch.nn.functional.silu(g) * u) @ Wt[E + s][2].t()
-            y += ys.float() * (sw[:, s:s + 1] if sw is not None else 1.0)
+            y += ys[s].float() * (sw[:, s:s + 1] if sw is not None else 1.0)
         return y.to(torch.bfloat16)
 
     for _ in range(3):
@@ -206,15 +224,58 @@ def allmax(v, ws):
     return float(t.item())
 
 
-def cpu_oracle_tokens_per_s(cfg, table, weights, x, ids, w, sw, sample):
-    """The oracle as it stands (oracle.moe.moe_block, fp64 NumPy) on `sample` tokens; setup untimed."""
-    from oracle.moe import moe_block, quantize_layer
-    ol = quantize_layer(weights, table, cfg.n_routed, cfg.n_shared)
-    rows = np.arange(sample)
-    t0 = time.perf_counter()
-    moe_block(x[rows], ol, ids[rows], w[rows], None if sw is None else sw[rows])
-    dt = time.perf_counter() - t0
-    return sample / dt, dt
+def _oracle_block(args):
+    """One block of oracle.moe.quantize_block (setup of the CPU baseline, run in a process pool)."""
+    from oracle.moe import quantize_block
+    wb, sch = args
+    qb = quantize_block(wb, sch)
+    if qb.w_bits != 16:  # same integer values in a compact dtype (the oracle casts codes to fp64 where it uses them)
+        qb.codes = qb.codes.astype(np.int8 if qb.codes.min() >= -128 and qb.codes.max() <= 127 else np.int16)
+    return qb
+
+
+def oracle_layer(cfg, table, weights, experts=None):
+    """The oracle's quantized layer (oracle.moe.QuantizedLayer), blocks quantized in parallel on the host cores.
+    `experts`: routed experts to quantize (others stay None: the sample never routes to them)."""
+    from concurrent.futures import ProcessPoolExecutor
+    from oracle.moe import QuantizedLayer
+    E, S = cfg.n_routed, cfg.n_shared
+    todo = [v for v in range(E + S) if experts is None or v >= E or v in experts]
+    jobs = [(weights[v][j], table[v][j]) for v in todo for j in range(3)]
+    with ProcessPoolExecutor(max(1, min(len(jobs), len(os.sched_getaffinity(0))))) as ex:
+        qbs = list(ex.map(_oracle_block, jobs, chunksize=1))
+    blocks = [None] * (E + S)
+    for i, v in enumerate(todo):
+        blocks[v] = qbs[3 * i: 3 * i + 3]
+    return QuantizedLayer(E, S, cfg.hidden, cfg.inter, cfg.shared_inter if S else 0, blocks)
+
+
+def cpu_oracle_baseline(cfg, table, weights, x, ids, w, sw, T, n_big):
+    """The oracle as it stands (oracle.moe.moe_block, fp64 NumPy) on two seeded token samples of this batch.
+
+    Every moe_block call converts the weights of each expert it touches (dequantized / fp64 codes), a fixed
+    cost per call, then spends a per-token cost; two sample sizes that touch the same experts separate the two
+    and give the extrapolated full-batch rate. Setup (quantizing the layer) is untimed."""
+    from oracle.moe import moe_block
+    ol = oracle_layer(cfg, table, weights)
+    rng = np.random.default_rng(5)
+    pts = []
+    for n in (max(1, n_big // 4), n_big):
+        rows = np.sort(rng.choice(T, min(n, T), replace=False))
+        t0 = time.perf_counter()
+        moe_block(x[rows], ol, ids[rows], w[rows], None if sw is None else sw[rows])
+        pts.append((len(rows), time.perf_counter() - t0, len(set(ids[rows].reshape(-1).tolist()) - {-1})))
+    (n1, t1, e1), (n2, t2, e2) = pts
+    per_tok = max((t2 - t1) / (n2 - n1), 1e-9) if n2 > n1 else t2 / n2
+    fixed = max(t2 - per_tok * n2, 0.0)
+    return {"value": n2 / t2, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"{n2} seeded random tokens of the {cfg.name} T={T} batch (oracle.moe.moe_block, fp64 NumPy): "
+                      f"{t2:.1f} s, {e2}/{cfg.n_routed} routed experts + {cfg.n_shared} shared touched",
+            "second_sample": {"tokens": n1, "s": t1, "experts_touched": e1},
+            "per_call_weight_conversion_s": fixed, "per_token_s": per_tok,
+            "extrapolated_full_batch_tokens_per_s": T / (fixed + per_tok * T),
+            "note": "value = measured sample throughput; the extrapolation charges the per-call weight conversion "
+                    "once per batch"}
 
 
 def run_reference(args, cfg, T):
@@ -227,9 +288,11 @@ def run_reference(args, cfg, T):
     x = gen_activations(T, cfg.hidden, seed=1)
     ids, w = gen_routing(T, cfg.n_routed, cfg.top_k, seed=0)
     sw = gen_shared_weights(T, cfg.n_shared) if cfg.n_shared else None
-    from oracle.moe import moe_block, quantize_layer
-    ol = quantize_layer(weights, table, cfg.n_routed, cfg.n_shared)
-    sample = max(1, min(T, args.cpu_sample // 4))
+    from oracle.moe import moe_block
+    ol = oracle_layer(cfg, table, weights)
+    # per step: a few random tokens (each call re-converts the weights of every expert it touches, so the step
+    # cost is dominated by that fixed part on the big layers; sized so K + W steps end within a few minutes)
+    sample = max(1, min(T, args.cpu_sample // (64 if cfg.name == "q2" else 8)))
     rng = np.random.default_rng(5)
     times = []
     for i in range(args.warmup + args.steps):
@@ -251,8 +314,22 @@ def run_reference(args, cfg, T):
     print(json.dumps(line), flush=True)
 
 
+def maybe_spawn(args) -> bool:
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run with N local ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    maybe_spawn(args)
     cfg = C.get_config(args.config)
     T = args.tokens or cfg.tokens
     if args.impl == "reference":
@@ -369,21 +446,35 @@ def main():
     else:
         counts = np.bincount(ids_np[ids_np >= 0].reshape(-1), minlength=cfg.n_routed)
         rl = layer_roofline(table, counts, cfg.hidden, cfg.inter, cfg.shared_inter, cfg.n_routed, T, peaks)
-    i8_dom = rl["flops_i8"] > rl["flops_bf16"]
-    peak_tf = peaks["i8_tops"] if i8_dom else peaks["bf16_tflops"]
-    achieved = rl["flops"] / (gemm_ms / 1e3) / 1e12
-    traffic = None
+    # bound of the dominant kernel from its own per-expert roofline: compute (FLOPs at each block's kind peak)
+    # vs bytes over HBM; the peak is the FLOP-mix one (FLOPs / sum_kind FLOPs_kind / peak_kind)
+    hbm_bound = rl["t_memory"] > rl["t_compute"]
+    if hbm_bound:
+        achieved = rl["bytes"] / (gemm_ms / 1e3) / 1e9
+        peak, unit, alg = peaks["hbm_gbs"], "GB/s", {"algorithmic_bytes_per_launch": rl["bytes"]}
+        peak_src = f"MEASURED_PEAKS.json hbm_gbs ({peaks['source']})"
+    else:
+        achieved = rl["flops"] / (gemm_ms / 1e3) / 1e12
+        peak, unit, alg = rl["peak_mix"] / 1e12, "TFLOP/s", {"algorithmic_flops_per_launch": rl["flops"]}
+        peak_src = (f"FLOP-mix of bf16 {peaks['bf16_tflops']:.0f} (MEASURED_PEAKS.json burst), i8 {peaks['i8_tops']:.0f} "
+                    f"({peaks['i8_source']}), f8 {peaks['f8_tflops']:.0f} ({peaks['f8_source']}); FLOP shares bf16 "
+                    f"{rl['flops_bf16'] / rl['flops']:.2f} / i8 {rl['flops_i8'] / rl['flops']:.2f} / f8 "
+                    f"{rl['flops_f8'] / rl['flops']:.2f}")
+    traffic, traffic_note = None, "no ncu capture of this library build for this config"
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s" if not i8_dom else "TOP/s",
-                "frac": achieved / peak_tf, "traffic": traffic, "kernel": "moe_gemm_kernel",
-                "peak_source": (peaks["i8_source"] if i8_dom else f"MEASURED_PEAKS.json bf16_tflops (burst, "
-                                                                    f"{peaks['source']})"),
-                "algorithmic_flops_per_launch": rl["flops"], "kernel_ms": gemm_ms}
+            tj = json.load(f)
+        if tj.get("lib_sha1") == lib_sha1() and tj.get("tokens") == T:
+            traffic, traffic_note = tj.get("dram_bytes_per_launch"), f"ncu --set full capture ({tp}, same library)"
+        else:
+            traffic_note = f"stale: {tp} was captured on another library build; not reported"
+    roofline = {"bound": "hbm" if hbm_bound else "tensor", "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note, "kernel": "moe_gemm_kernel",
+                "peak_source": peak_src, **alg, "kernel_ms": gemm_ms}
     per_expert = {"t_roof_us": rl["t_roof"] * 1e6, "frac_of_gemm": rl["t_roof"] / (gemm_ms / 1e3),
-                  "frac_of_step": rl["t_roof"] / (ms / 1e3), "alg_bytes": rl["bytes"]}
+                  "frac_of_step": rl["t_roof"] / (ms / 1e3), "alg_bytes": rl["bytes"], "alg_flops": rl["flops"],
+                  "t_compute_us": rl["t_compute"] * 1e6, "t_memory_us": rl["t_memory"] * 1e6}
     stage_ms = {n: float(stages[:, i].mean()) for i, n in enumerate(["route", "gather", "plan", "gemm", "combine"])}
 
     comparators = None
@@ -413,16 +504,13 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        samp = min(T, args.cpu_sample)
-        tps, dt = cpu_oracle_tokens_per_s(cfg, table, weights, x_np, ids_np, w_np, sw_np, samp)
-        cpu = {"value": tps, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-               "sample": f"first {samp} tokens of the {cfg.name} T={T} batch (oracle.moe.moe_block, fp64), "
-                         f"{dt:.1f} s"}
+        cpu = cpu_oracle_baseline(cfg, table, weights, x_np, ids_np, w_np, sw_np, T, min(T, args.cpu_sample))
     launches = layer.kernels_per_call
     if use_ep:  # ep_route + ep_pack + local layer + shared layer + ep_combine (NCCL kernels not counted)
         launches += 3 + (ep.shared.kernels_per_call if ep.shared is not None else 0)
     if rank == 0:
-        dt = "int8" if i8_dom else "bf16"
+        kinds = [k for k in ("bf16", "i8", "f8") if rl["flops_" + k] > 0]
+        dt = "+".join({"bf16": "bf16", "i8": "int8", "f8": "e4m3"}[k] for k in kinds)
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dt,
                 "data": "synthetic (seeded N(0,1) x, N(0,1/K) weights, Zipf-0.8 Gumbel top-k routing)",

@@ -103,12 +103,18 @@ def wa_int_accumulators(qa: np.ndarray, qw: np.ndarray, group: int) -> np.ndarra
     return out
 
 
-def linear_block(xin: np.ndarray, blk: QBlock) -> np.ndarray:
-    """y[m, n] for block input xin[m, K] (bf16-valued float64). fp64 result."""
+def linear_block(xin: np.ndarray, blk: QBlock, exact_weights: bool = False) -> np.ndarray:
+    """y[m, n] for block input xin[m, K] (bf16-valued float64). fp64 result.
+
+    exact_weights: weight-only blocks multiply by the exact dequantized ŵ = q·s + z of P:53 instead of its
+    bf16 rounding (reading R5); used to check the GPU against the paper's exact dequantization too.
+    """
     xin = np.asarray(xin, dtype=np.float64)
     if blk.w_bits == 16:
         return xin @ bits_to_f64(blk.codes).T
     if blk.a_bits == 16:  # weight-only: dequantized weights rounded once to bf16 (reading R5)
+        if exact_weights:
+            return xin @ dequantize_weight(blk.codes, blk.scale, blk.zero, blk.w_group).T
         return xin @ dequantize_weight_bf16(blk).T
     qa, sa, _ = quantize_act(xin.astype(np.float32), blk.a_bits, blk.a_group)
     acc = wa_int_accumulators(qa, blk.codes, blk.w_group)
@@ -122,13 +128,14 @@ def silu(v):
     return v / (1.0 + np.exp(-v))
 
 
-def expert_ffn(xe: np.ndarray, gate: QBlock, up: QBlock, down: QBlock, return_h: bool = False):
+def expert_ffn(xe: np.ndarray, gate: QBlock, up: QBlock, down: QBlock, return_h: bool = False,
+               exact_weights: bool = False):
     """Eq. 1: W_down(σ(W_gate X) ⊙ W_up X), h rounded to bf16 (R16)."""
-    g = linear_block(xe, gate)
-    u = linear_block(xe, up)
+    g = linear_block(xe, gate, exact_weights)
+    u = linear_block(xe, up, exact_weights)
     with np.errstate(over="ignore"):
         h = bf16_round_f64(silu(g) * u)
-    o = linear_block(h, down)
+    o = linear_block(h, down, exact_weights)
     return (o, h) if return_h else o
 
 
@@ -154,7 +161,7 @@ def quantize_layer(weights, table, n_routed: int, n_shared: int) -> QuantizedLay
 
 
 def moe_block(x_bits: np.ndarray, layer: QuantizedLayer, topk_ids: np.ndarray, topk_w: np.ndarray,
-              shared_w: Optional[np.ndarray] = None) -> np.ndarray:
+              shared_w: Optional[np.ndarray] = None, exact_weights: bool = False) -> np.ndarray:
     """F = Σ_e w_e ⊙ expert_e(X_e) (Eq. 2) + Σ_s shared_w[:, s] ⊙ shared_s(X); fp64 [T, d].
 
     Routes with id −1 are skipped; duplicate ids in a token are legal and each
@@ -169,11 +176,11 @@ def moe_block(x_bits: np.ndarray, layer: QuantizedLayer, topk_ids: np.ndarray, t
         tt, jj = np.nonzero(ids == e)  # row-major: (t, j) order
         if tt.size == 0:
             continue
-        o = expert_ffn(x[tt], *layer.blocks[e])
+        o = expert_ffn(x[tt], *layer.blocks[e], exact_weights=exact_weights)
         for r in range(tt.size):
             y[tt[r]] += w[tt[r], jj[r]] * o[r]
     for s in range(layer.n_shared):
-        o = expert_ffn(x, *layer.blocks[layer.n_routed + s])
+        o = expert_ffn(x, *layer.blocks[layer.n_routed + s], exact_weights=exact_weights)
         ws = np.ones(T) if shared_w is None else np.asarray(shared_w, dtype=np.float64)[:, s]
         y += ws[:, None] * o
     return y

@@ -183,19 +183,31 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
   const int e1 = block_excl_scan(c1, s_wt, &t1);
   const int eq = block_excl_scan(cq, s_wt, &tq);
   int e2 = block_excl_scan(c2, s_wt, &t2);
-  // split-K of the downs when they cannot fill the SMs (common.cuh); red_cnt == nullptr: not allowed
-  __shared__ int s_minns;
+  // split-K of the downs when they cannot fill the SMs (common.cuh); red_cnt == nullptr: not allowed.
+  // One slice count S for every splittable down of the launch (the last-arriver reduce counts S arrivals), so
+  // S must give every splittable expert a non-empty last slice (experts may differ in ns: shared_inter != inter)
+  // and the shortest one at least 2 stages.
+  __shared__ int s_minns, s_ok;
   if (tid == 0) s_minns = 1 << 30;
   __syncthreads();
-  if (tid < V && down_splittable(ex[tid])) atomicMin(&s_minns, ex[tid].blk[2].geo.ns);
+  const bool splittable_v = tid < V && down_splittable(ex[tid]);
+  if (splittable_v) atomicMin(&s_minns, ex[tid].blk[2].geo.ns);
   __syncthreads();
   int S = 1;
   if (red_cnt != nullptr && t2 > 0 && t2 < kNumSms && s_minns < (1 << 30)) {
-    S = min(kSplitMax, (kNumSms + t2 - 1) / t2);
-    for (; S > 1; --S) {
-      int a, b;
-      split_range(s_minns, S, S - 1, a, b);
-      if (b - a >= 2) break;
+    for (S = min(kSplitMax, (kNumSms + t2 - 1) / t2); S > 1; --S) {
+      if (tid == 0) s_ok = 1;
+      __syncthreads();
+      if (splittable_v) {
+        int a, b;
+        split_range(ex[tid].blk[2].geo.ns, S, S - 1, a, b);
+        const int need = ex[tid].blk[2].geo.ns == s_minns ? 2 : 1;
+        if (b - a < need) atomicAnd(&s_ok, 0);
+      }
+      __syncthreads();
+      const int ok = s_ok;
+      __syncthreads();
+      if (ok) break;
     }
   }
   if (S > 1) {

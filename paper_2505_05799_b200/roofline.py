@@ -25,14 +25,29 @@ def load_peaks() -> Dict[str, float]:
         out.update({k: float(m[k]) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
         out["source"] = "measured"
     q = os.path.join(ROOT, "profiles", "i8_peak.json")
+    m8 = {}
     if os.path.exists(q):
         with open(q) as f:
-            out["i8_tops"] = float(json.load(f)["i8_tops"])
+            m8 = json.load(f)
+    if m8.get("i8_tops"):
+        out["i8_tops"] = float(m8["i8_tops"])
         out["i8_source"] = "measured (profiles/i8_peak.json, torch._int_mm 8192^3)"
     else:
         out["i8_tops"] = 2.0 * out["bf16_tflops"]
         out["i8_source"] = "assumed 2 x bf16 (B200 nominal ratio 4.5/2.25)"
+    # w4a4 runs on kind::f8f6f4 (e4m3): its own measured peak, else the i8 figure (same nominal 4.5 PF dense)
+    if m8.get("f8_tflops"):
+        out["f8_tflops"] = float(m8["f8_tflops"])
+        out["f8_source"] = "measured (profiles/i8_peak.json, torch._scaled_mm e4m3 8192^3)"
+    else:
+        out["f8_tflops"] = out["i8_tops"]
+        out["f8_source"] = "assumed = i8 (B200 nominal fp8 = int8 = 4.5 PF dense)"
     return out
+
+
+def kind_peak(kind: str, peaks) -> float:
+    """Tensor peak (FLOP/s) of an MMA kind: bf16 (kind::f16), i8 (w5a5 / w8a8), f8 (w4a4 on kind::f8f6f4)."""
+    return {"bf16": peaks["bf16_tflops"], "i8": peaks["i8_tops"], "f8": peaks.get("f8_tflops", peaks["i8_tops"])}[kind] * 1e12
 
 
 def crossover_m(peak_a: float, bytes_per_w_b: float, bw: float) -> float:
@@ -52,18 +67,19 @@ def block_roofline(m: int, n: int, k: int, w_bits: int, a_bits: int, w_group: in
         g = k if w_group == -1 else w_group
         wbytes = n * k * w_bits / 8.0
         meta = n * (k / g) * 2.0 * (1 if (sym or a_bits != 16) else 2)
-        kind = "bf16" if a_bits == 16 else "i8"
+        kind = "bf16" if a_bits == 16 else ("f8" if w_bits == 4 else "i8")
     abytes = m * k * (2.0 if a_bits == 16 else 1.0) + (0 if a_bits == 16 else m * max(1, k // 128) * 4.0)
     obytes = m * n * 2.0
     byt = wbytes + meta + abytes + obytes
-    P = (peaks["bf16_tflops"] if kind == "bf16" else peaks["i8_tops"]) * 1e12
+    P = kind_peak(kind, peaks)
     t = max(flops / P, byt / (peaks["hbm_gbs"] * 1e9))
-    return {"flops": flops, "bytes": byt, "t": t, "kind": kind}
+    return {"flops": flops, "bytes": byt, "t": t, "kind": kind, "t_compute": flops / P}
 
 
 def layer_roofline(table, counts, hidden: int, inter: int, shared_inter: int, n_routed: int, T: int, peaks) -> Dict:
     """Sum of per-(expert, block) rooflines (seconds) + totals; shared experts see m = T."""
-    tot = {"t_roof": 0.0, "flops": 0.0, "bytes": 0.0, "flops_bf16": 0.0, "flops_i8": 0.0}
+    tot = {"t_roof": 0.0, "flops": 0.0, "bytes": 0.0, "flops_bf16": 0.0, "flops_i8": 0.0, "flops_f8": 0.0,
+           "t_compute": 0.0, "t_memory": 0.0}
     for v, row in enumerate(table):
         m = int(counts[v]) if v < n_routed else T
         if m == 0:
@@ -76,4 +92,8 @@ def layer_roofline(table, counts, hidden: int, inter: int, shared_inter: int, n_
             tot["flops"] += r["flops"]
             tot["bytes"] += r["bytes"]
             tot["flops_" + r["kind"]] += r["flops"]
+            tot["t_compute"] += r["t_compute"]
+            tot["t_memory"] += r["bytes"] / (peaks["hbm_gbs"] * 1e9)
+    # the FLOP-mix peak: the rate at which the whole block's FLOPs would run if every block ran at its kind's peak
+    tot["peak_mix"] = tot["flops"] / tot["t_compute"] if tot["t_compute"] > 0 else 0.0
     return tot

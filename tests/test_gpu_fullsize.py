@@ -52,14 +52,14 @@ def _sampled_case(cfg, table, T, P, max_rows=16, seed=0):
     return case, ol, rows
 
 
-def _check(case, ol, rows):
+def _check(case, ol, rows, exact_weights=False):
     layer = gpu_layer(case)
     y = gpu_run(layer, case)
     assert np.isfinite(y).all(), f"non-finite rows: {np.nonzero(~np.isfinite(y).all(1))[0][:16]}"
     n, ex = layer.task_stats(case["T"], case["k"])
     assert n > 0 and ex == n and layer.poll_error() == 0, (n, ex)
     sw = None if case["shared_w"] is None else case["shared_w"][rows]
-    ref = moe_block(case["x"][rows], ol, case["ids"][rows], case["w"][rows], sw)
+    ref = moe_block(case["x"][rows], ol, case["ids"][rows], case["w"][rows], sw, exact_weights=exact_weights)
     return row_rel_err(y[rows], ref)
 
 
@@ -124,5 +124,31 @@ def test_q15_full_size(mx):
     cnt = np.bincount(ids.ravel(), minlength=cfg.n_routed)
     P = np.argsort(-cnt)[:10].tolist()
     case, ol, rows = _sampled_case(cfg, table, cfg.tokens, P)
+    e = _check(case, ol, rows)
+    assert e <= TOL, e
+
+
+def test_dsv2_exact_dequant(mx):
+    """DSV2 weight-only mix against the oracle with the paper's EXACT dequantized weights q*s + z, not
+    their bf16 rounding (reading R5): the GPU's bf16 operand rounding stays inside the 1e-2 gate."""
+    cfg = C.get_config("dsv2")
+    table = C.precision_table(cfg)
+    ids, _ = gen_routing(cfg.tokens, cfg.n_routed, cfg.top_k, seed=0)
+    cnt = np.bincount(ids.ravel(), minlength=cfg.n_routed)
+    P = np.argsort(-cnt)[:14].tolist()
+    case, ol, rows = _sampled_case(cfg, table, cfg.tokens, P)
+    e = _check(case, ol, rows, exact_weights=True)
+    assert e <= TOL, e
+
+
+def test_mixtral_t16384(mx):
+    """Mixtral-8x7B at the top of the token sweep, T = 16384 (compute-bound: every expert w8a8), sampled rows."""
+    cfg = C.get_config("mx")
+    T = 16384
+    table = C.precision_table(cfg, T)
+    ids, _ = gen_routing(T, cfg.n_routed, cfg.top_k, seed=0)
+    cnt = np.bincount(ids.ravel(), minlength=cfg.n_routed)
+    P = np.argsort(-cnt)[:2].tolist()
+    case, ol, rows = _sampled_case(cfg, table, T, P, max_rows=8)
     e = _check(case, ol, rows)
     assert e <= TOL, e

@@ -131,3 +131,17 @@ def test_split_k_downs(mx):
         e, layer, y = _parity(case)
         assert e <= TOL, (T, e)
         assert np.array_equal(gpu_run(layer, case), y)
+
+
+def test_split_k_unequal_shared_inter(mx):
+    """Split-K with downs of different stage counts in one launch (routed inter 1024 = 16 bf16-kind stages, shared
+    inter 1152 = 18): one slice count must leave no expert an empty last slice (S=4 gave ns=18 the
+    empty slice [18, 18) and hung the persistent kernel)."""
+    cfg = C.LayerConfig("splitk2", 4, 1, 512, 1024, 1152, 2, 8)
+    wo = C.WO(4, 128)
+    table = [[wo, wo, C.WO(2, -1)], [wo, wo, wo], [C.WA(8, -1)] * 3, [wo, wo, C.WO(3, 128)], [wo, wo, C.WO(4, -1)]]
+    for T in (1, 3, 8):
+        case = make_case(cfg, table, T, seed=T)
+        e, layer, y = _parity(case)
+        assert e <= TOL, (T, e)
+        assert np.array_equal(gpu_run(layer, case), y)

@@ -84,16 +84,19 @@ def test_wo_linear_bruteforce(sch):
     X = ob.bits_to_f64(_rand_bf16(rng, (M, K)))
     blk = quantize_block(W, sch)
     y = linear_block(X, blk)
+    y_exact = linear_block(X, blk, exact_weights=True)
     g = K if sch.w_group == -1 else sch.w_group
     for m in range(M):
         for n in range(N):
-            acc = Fraction(0)
+            acc, acc_x = Fraction(0), Fraction(0)
             for k in range(K):
                 wq = int(blk.codes[n, k]) * Fraction(blk.scale[n, k // g])
                 if blk.zero is not None:
                     wq += Fraction(blk.zero[n, k // g])
                 acc += Fraction(X[m, k]) * _bf16_round_exact(wq)  # reading R5: bf16 dequantized weight
+                acc_x += Fraction(X[m, k]) * wq                   # the exact dequantized weight
             assert abs(float(acc) - y[m, n]) <= 1e-12 * max(1.0, abs(float(acc)))
+            assert abs(float(acc_x) - y_exact[m, n]) <= 1e-12 * max(1.0, abs(float(acc_x)))
 
 
 @pytest.mark.parametrize("sch", [C.WA(8, -1), C.WA(4, 128), C.WA(5, 128), C.WA(4, -1)])
@@ -212,3 +215,50 @@ def test_table6_counts():
     assert sum(1 for b in flat if (b.w_bits, b.w_group) == (4, -1)) == 18
     assert all(r[0] == r[1] for r in rows)
     assert all(b.a_group == b.w_group and b.a_bits == b.w_bits for b in flat)
+
+
+def test_shared_experts_pin():
+    """Shared-expert branch of moe_block pinned to an independent torch fp64 computation (reading R13): every token
+    gets sum_j w[t,j] MLP_ids[t,j](x_t) + sum_s shared_w[t,s] MLP_shared_s(x_t), with S = 2 shared experts of their own
+    width, non-uniform per-token shared weights, dead routes (-1) and a token with no routed expert at all."""
+    rng = np.random.default_rng(11)
+    E, S, d, f, fs, T, k = 3, 2, 64, 128, 192, 11, 2
+    W = [[_rand_bf16(rng, (ff, d), 0.2), _rand_bf16(rng, (ff, d), 0.2), _rand_bf16(rng, (d, ff), 0.2)]
+         for ff in [f] * E + [fs] * S]
+    layer = quantize_layer(W, [[C.W16] * 3] * (E + S), E, S)
+    assert layer.shared_inter == fs
+    X = _rand_bf16(rng, (T, d))
+    ids = rng.integers(-1, E, (T, k))
+    ids[4] = -1
+    w = rng.uniform(0.1, 1.0, (T, k)).astype(np.float32)
+    sw = rng.uniform(-0.5, 1.5, (T, S)).astype(np.float32)
+    y = moe_block(X, layer, ids, w, sw)
+
+    t = lambda b: torch.from_numpy(ob.bits_to_f64(b))
+    x = t(X)
+
+    def mlp(v, xs):
+        h = torch.nn.functional.silu(xs @ t(W[v][0]).T) * (xs @ t(W[v][1]).T)
+        h = h.to(torch.float32).to(torch.bfloat16).to(torch.float64)
+        return h @ t(W[v][2]).T
+
+    ref = torch.zeros(T, d, dtype=torch.float64)
+    for tt in range(T):
+        for j in range(k):
+            if ids[tt, j] >= 0:
+                ref[tt] += float(w[tt, j]) * mlp(int(ids[tt, j]), x[tt:tt + 1])[0]
+    for s in range(S):
+        ref += torch.from_numpy(sw[:, s].astype(np.float64))[:, None] * mlp(E + s, x)
+    ref = ref.numpy()
+    assert np.max(np.abs(y - ref)) <= 1e-2 * np.max(np.abs(ref))
+    # the token without routed experts is exactly its shared part; shared weights enter linearly per expert
+    only_shared = moe_block(X[4:5], layer, ids[4:5], w[4:5], sw[4:5])
+    assert np.allclose(only_shared[0], y[4], rtol=0, atol=0)
+    sw2 = sw.copy()
+    sw2[:, 1] *= 2.0
+    y2 = moe_block(X, layer, ids, w, sw2)
+    sw0 = sw.copy()
+    sw0[:, 1] = 0.0
+    y0 = moe_block(X, layer, ids, w, sw0)
+    assert np.allclose(y2 - y, y - y0, rtol=1e-12, atol=1e-12)
+    assert np.max(np.abs(y - y0)) > 1e-3  # shared expert 1 contributes
