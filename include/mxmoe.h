@@ -110,7 +110,11 @@ typedef struct mxm_layer mxm_layer;
 /* [sync] device bytes needed for the layer's descriptor table. */
 mxm_status mxm_layer_desc_bytes(const mxm_layer_desc* d, int64_t* bytes);
 /* [sync] validate every block, upload the descriptor table into desc_dev (caller-owned device buffer of
- * mxm_layer_desc_bytes bytes), return a host handle. tile_costs: NULL = analytic LPT cost model. */
+ * mxm_layer_desc_bytes bytes), return a host handle. tile_costs: NULL = analytic LPT cost model, else a HOST
+ * float array [(n_routed + n_shared) * 4]: the measured cost (ms) of one m-tile group of each expert at token
+ * tiles 16 / 32 / 64 / 96 (the output of mxm_profile_tile_costs; entries <= 0 fall back to the analytic model).
+ * The planner orders m-tile groups by this cost, longest first (greedy LPT, "pre-profiled single-tile
+ * runtime costs"). */
 mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_bytes, const void* tile_costs,
                           mxm_layer** out);
 void mxm_layer_free(mxm_layer* l);
@@ -130,6 +134,19 @@ mxm_status mxm_workspace_bytes(const mxm_layer* l, int64_t max_tokens, int32_t t
 mxm_status mxm_moe_group_gemm(const mxm_layer* l, const void* x, int64_t T, int32_t top_k, const int32_t* topk_ids,
                               const float* topk_w, const float* shared_w, void* y, void* workspace, int64_t ws_bytes,
                               mxm_stream stream);
+/* Tile-cost profiling (the cost model and scheduler use pre-profiled single-tile runtime costs).
+ * [sync] bytes of the caller-owned device scratch mxm_profile_tile_costs needs (a workspace for 96 tokens plus
+ * its inputs and output). */
+mxm_status mxm_profile_scratch_bytes(const mxm_layer* l, int64_t* bytes);
+/* [sync] measure, on this GPU, the cost of one m-tile group of every expert at each token tile (16, 32, 64, 96;
+ * capped at the expert's largest tile): the persistent group-GEMM is launched on ONE CTA over zero inputs routed
+ * to that expert only (split-K off), timed with CUDA events, best of 3, minus the same run with no routed token
+ * (shared experts only; their cost is that run divided by n_shared). costs: HOST float [(n_routed+n_shared)*4], ms. */
+mxm_status mxm_profile_tile_costs(const mxm_layer* l, void* scratch, int64_t scratch_bytes, float* costs,
+                                  mxm_stream stream);
+/* [sync] replace the layer's tile-cost table (HOST float [(n_routed+n_shared)*4], ms; NULL = analytic model). */
+mxm_status mxm_layer_set_tile_costs(mxm_layer* l, const float* costs);
+
 /* [sync] read (and clear) the device error word of the last call using `workspace`: *code = MXM_OK or MXM_E_DATA. */
 mxm_status mxm_poll_device_error(const mxm_layer* l, const void* workspace, mxm_stream stream, int32_t* code);
 /* Test/debug [sync]: number of tile tasks (gate/up, h-quant, down) the planner emitted in the last call

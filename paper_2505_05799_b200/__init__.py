@@ -243,6 +243,27 @@ class MoELayer:
         n_gu = 2 * (d // 128) * R * F
         return y, ws, acc[:n_gu].view(2, d // 128, R, F), acc[n_gu:].view(F // 128, R, d)
 
+    def profile_tile_costs(self):
+        """Measured m-tile group costs (ms) [V, 4] for token tiles 16/32/64/96 (mxm_profile_tile_costs)."""
+        import numpy as np
+        nb = C.c_int64()
+        check(load().mxm_profile_scratch_bytes(self._h, C.byref(nb)))
+        scratch = torch.empty(nb.value, dtype=torch.uint8, device=self._desc_dev.device)
+        V = self.n_routed + self.n_shared
+        out = (C.c_float * (4 * V))()
+        check(load().mxm_profile_tile_costs(self._h, _ptr(scratch), nb.value, out, _stream()))
+        return np.frombuffer(out, dtype=np.float32).reshape(V, 4).copy()
+
+    def set_tile_costs(self, costs):
+        """Use a measured cost table [V, 4] (ms) as the planner's LPT key (None: the analytic model)."""
+        import numpy as np
+        if costs is None:
+            check(load().mxm_layer_set_tile_costs(self._h, None))
+            return
+        arr = np.ascontiguousarray(costs, dtype=np.float32).reshape(-1)
+        assert arr.size == 4 * (self.n_routed + self.n_shared)
+        check(load().mxm_layer_set_tile_costs(self._h, arr.ctypes.data_as(C.c_void_p)))
+
     def profile(self, n_slots: int):
         """Record per-stage CUDA events for the next calls (ring of n_slots calls)."""
         check(load().mxm_layer_profile(self._h, n_slots))

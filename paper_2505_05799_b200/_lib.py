@@ -69,6 +69,9 @@ SIGNATURES = {
     "mxm_debug_workspace_layout": (C.c_int, [_P, _I64, _I32, C.POINTER(_I64)]),
     "mxm_debug_acc_bytes": (C.c_int, [_P, _I64, _I32, C.POINTER(_I64)]),
     "mxm_debug_moe_group_gemm_dump": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _I64, _P, _I64, _P]),
+    "mxm_profile_scratch_bytes": (C.c_int, [_P, C.POINTER(_I64)]),
+    "mxm_profile_tile_costs": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "mxm_layer_set_tile_costs": (C.c_int, [_P, _P]),
     "mxm_last_error": (C.c_char_p, []),
     "mxm_version": (C.c_char_p, []),
 }

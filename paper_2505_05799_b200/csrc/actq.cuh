@@ -10,16 +10,11 @@ namespace mxm {
 
 __device__ __forceinline__ float bf16_bits_to_float(uint32_t b) { return __uint_as_float(b << 16); }
 
+// warp max of non-negative floats (|v|): their bit patterns order like the values, so one REDUX.MAX does it
 __device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+  return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
 }
-__device__ __forceinline__ int warp_sum(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+__device__ __forceinline__ int warp_sum(int v) { return __reduce_add_sync(0xffffffffu, v); }
 
 // Code byte of an integer code q (|q| <= 127): two's complement int8 (kind::i8 operands, canonical output), or
 // for E4 the e4m3 byte (q<0)<<7 | |q| whose value is q * 2^-9 (|q| <= 15; kind::f8f6f4 operands of w4a4 blocks).

@@ -259,7 +259,6 @@ mxm_status mxm_layer_desc_bytes(const mxm_layer_desc* d, int64_t* bytes) {
 
 mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_bytes, const void* tile_costs,
                           mxm_layer** out) {
-  (void)tile_costs;
   if (!d || !d->blocks || !desc_dev || !out) return fail(MXM_E_CONFIG, "null argument");
   const int E = d->n_routed, S = d->n_shared, V = E + S;
   if (E <= 0 || E > 256 || S < 0 || S > 32 || V > 256) return fail(MXM_E_CONFIG, "expert count out of range");
@@ -325,6 +324,11 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
     }
     if (e.blk[2].in_slot == 1) l->need_hq = true;
   }
+  if (tile_costs) {  // measured per-(expert, token tile) m-tile group costs (mxm_profile_tile_costs), ms
+    const float* c = reinterpret_cast<const float*>(tile_costs);
+    for (int v = 0; v < V; ++v)
+      for (int i = 0; i < 4; ++i) l->ex[v].cost[i] = c[v * 4 + i] > 0.f ? c[v * 4 + i] : 0.f;
+  }
   cudaError_t ce = cudaMemcpy(desc_dev, l->ex.data(), sizeof(ExpertDesc) * V, cudaMemcpyHostToDevice);
   if (ce != cudaSuccess) {
     delete l;
@@ -348,9 +352,18 @@ mxm_status mxm_workspace_bytes(const mxm_layer* l, int64_t max_tokens, int32_t t
 
 // The launch sequence of one MoE block; `dump` != nullptr selects the test-only accumulator-dump kernel
 // (mxm_debug_moe_group_gemm_dump) and disables split-K so every accumulator is a whole-K (or whole-group) sum.
+// Tile-cost profiling (mxm_profile_tile_costs) runs the same sequence on one CTA (grid = 1) without split-K and
+// brackets the persistent GEMM launch with its own events.
+struct RunOpts {
+  int grid = 0;  // 0: one CTA per SM
+  bool no_split = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
 static mxm_status run_group_gemm(const mxm_layer* l, const void* x, int64_t T, int32_t k, const int32_t* topk_ids,
                                  const float* topk_w, const float* shared_w, void* y, void* ws, int64_t ws_bytes,
-                                 mxm_stream stream, uint32_t* dump) {
+                                 mxm_stream stream, uint32_t* dump, const RunOpts& opt = RunOpts()) {
+  const bool no_split = dump != nullptr || opt.no_split;
   if (!l || !ws || (T > 0 && (!x || !topk_ids || !topk_w || !y))) return fail(MXM_E_CONFIG, "null argument");
   if (k <= 0 || k > 32 || T < 0) return fail(MXM_E_CONFIG, "bad top_k / T");
   const WsLayout w = make_layout(l, T, k);
@@ -399,7 +412,7 @@ static mxm_status run_group_gemm(const mxm_layer* l, const void* x, int64_t T, i
   MXM_CUDA(cudaStreamWaitEvent(ml->side, ml->ev_fork, 0));
   MXM_CUDA(launch_plan(l->ex_dev, l->V, l->E, T, l->d, v_off, (int)w.g_max, w.task_cap, (Task*)P(w.tasks),
                        (int32_t*)P(w.meta), (int32_t*)P(w.grp_n1), (int32_t*)P(w.grp_nq), (int32_t*)P(w.p1_done),
-                       (int32_t*)P(w.hq_done), dump ? nullptr : (int32_t*)P(w.red_cnt), ml->side));
+                       (int32_t*)P(w.hq_done), no_split ? nullptr : (int32_t*)P(w.red_cnt), ml->side));
   MXM_CUDA(cudaEventRecord(ml->ev_join, ml->side));
   // S2 activation quantize + gather
   MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
@@ -442,13 +455,15 @@ static mxm_status run_group_gemm(const mxm_layer* l, const void* x, int64_t T, i
   prm.hmax = (uint32_t*)P(w.hmax);
   prm.O = (uint16_t*)P(w.O);
   prm.row_w = row_w;
-  prm.P = dump ? nullptr : (float*)P(w.P);
-  prm.red_cnt = dump ? nullptr : (int32_t*)P(w.red_cnt);
+  prm.P = no_split ? nullptr : (float*)P(w.P);
+  prm.red_cnt = no_split ? nullptr : (int32_t*)P(w.red_cnt);
   prm.dump = dump;
   prm.d = l->d;
   prm.f_max = l->f_max;
   prm.prof = reinterpret_cast<unsigned long long*>(l->prof_counters);
-  MXM_CUDA(launch_moe_gemm(prm, num_sms(), st));
+  if (opt.ev0) MXM_CUDA(cudaEventRecord(opt.ev0, st));
+  MXM_CUDA(launch_moe_gemm(prm, opt.grid > 0 ? opt.grid : num_sms(), st));
+  if (opt.ev1) MXM_CUDA(cudaEventRecord(opt.ev1, st));
   mark(4);
   // S8 combine
   MXM_CUDA(launch_combine(P(w.O), l->d, T, k, l->S, inv, y, st));
@@ -480,6 +495,84 @@ mxm_status mxm_debug_moe_group_gemm_dump(const mxm_layer* l, const void* x, int6
   if (s != MXM_OK) return s;
   if (!acc || acc_bytes < need) return fail(MXM_E_CONFIG, "accumulator dump buffer too small");
   return run_group_gemm(l, x, T, k, topk_ids, topk_w, shared_w, y, ws, ws_bytes, stream, (uint32_t*)acc);
+}
+
+static constexpr int kProfTiles[4] = {16, 32, 64, MXM_DUAL_TILE};
+
+mxm_status mxm_profile_scratch_bytes(const mxm_layer* l, int64_t* bytes) {
+  if (!l || !bytes) return fail(MXM_E_CONFIG, "null argument");
+  const int64_t T = MXM_DUAL_TILE;
+  *bytes = make_layout(l, T, 1).total + align256(2 * T * l->d) * 2 + align256(4 * T) * 2;
+  return MXM_OK;
+}
+
+mxm_status mxm_profile_tile_costs(const mxm_layer* l, void* scratch, int64_t scratch_bytes, float* costs,
+                                  mxm_stream stream) {
+  if (!l || !scratch || !costs) return fail(MXM_E_CONFIG, "null argument");
+  int64_t need = 0;
+  mxm_status s = mxm_profile_scratch_bytes(l, &need);
+  if (s != MXM_OK) return s;
+  if (scratch_bytes < need) return fail(MXM_E_CONFIG, "profile scratch too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t Tm = MXM_DUAL_TILE;
+  uint8_t* b = reinterpret_cast<uint8_t*>(scratch);
+  const int64_t wsb = make_layout(l, Tm, 1).total;
+  void* ws = b;
+  void* x = b + wsb;
+  void* y = b + wsb + align256(2 * Tm * l->d);
+  int32_t* ids = reinterpret_cast<int32_t*>(b + wsb + 2 * align256(2 * Tm * l->d));
+  float* w = reinterpret_cast<float*>(b + wsb + 2 * align256(2 * Tm * l->d) + align256(4 * Tm));
+  // inputs: zeros (tile cost does not depend on the values), unit route weights
+  MXM_CUDA(cudaMemsetAsync(x, 0, 2 * Tm * l->d, st));
+  std::vector<float> ones(Tm, 1.f);
+  MXM_CUDA(cudaMemcpyAsync(w, ones.data(), 4 * Tm, cudaMemcpyHostToDevice, st));
+  cudaEvent_t e0, e1;
+  MXM_CUDA(cudaEventCreate(&e0));
+  MXM_CUDA(cudaEventCreate(&e1));
+  RunOpts opt;
+  opt.grid = 1;  // single-CTA runs: the cost of one SM working through the group's tiles
+  opt.no_split = true;
+  opt.ev0 = e0;
+  opt.ev1 = e1;
+  std::vector<int32_t> hid(Tm);
+  auto timed = [&](int64_t T, int32_t id, float* ms) -> mxm_status {
+    for (int64_t t = 0; t < T; ++t) hid[t] = id;
+    MXM_CUDA(cudaMemcpyAsync(ids, hid.data(), 4 * T, cudaMemcpyHostToDevice, st));
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+      mxm_status r = run_group_gemm(l, x, T, 1, ids, w, nullptr, y, ws, wsb, stream, nullptr, opt);
+      if (r != MXM_OK) return r;
+      MXM_CUDA(cudaEventSynchronize(e1));
+      float m = 0.f;
+      MXM_CUDA(cudaEventElapsedTime(&m, e0, e1));
+      best = m < best ? m : best;
+    }
+    *ms = best;
+    return MXM_OK;
+  };
+  mxm_status r = MXM_OK;
+  for (int ni = 0; ni < 4 && r == MXM_OK; ++ni) {
+    float base = 0.f;  // shared experts only (every token routed nowhere)
+    r = timed(kProfTiles[ni], -1, &base);
+    for (int v = 0; v < l->E && r == MXM_OK; ++v) {
+      const int T = kProfTiles[ni] < tile_cap(l->ex[v]) ? kProfTiles[ni] : tile_cap(l->ex[v]);
+      float t = 0.f;
+      r = timed(T, v, &t);
+      costs[v * 4 + ni] = t - base > 1e-6f ? t - base : 1e-6f;
+    }
+    for (int v = l->E; v < l->V; ++v) costs[v * 4 + ni] = base / (float)l->S;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return r;
+}
+
+mxm_status mxm_layer_set_tile_costs(mxm_layer* l, const float* costs) {
+  if (!l) return fail(MXM_E_CONFIG, "null layer");
+  for (int v = 0; v < l->V; ++v)
+    for (int i = 0; i < 4; ++i) l->ex[v].cost[i] = costs && costs[v * 4 + i] > 0.f ? costs[v * 4 + i] : 0.f;
+  MXM_CUDA(cudaMemcpy(l->ex_dev, l->ex.data(), sizeof(ExpertDesc) * l->V, cudaMemcpyHostToDevice));
+  return MXM_OK;
 }
 
 mxm_status mxm_debug_workspace_layout(const mxm_layer* l, int64_t T, int32_t k, int64_t* off) {

@@ -71,6 +71,7 @@ struct ExpertDesc {
   int32_t dual;       // gate and up run as one K loop sharing the token tile (same MMA kind and input slot)
   int32_t shared;     // 1 = shared expert (all tokens)
   int32_t pad;
+  float cost[4];      // measured cost of one m-tile group at token tiles 16 / 32 / 64 / dual (ms; 0 = analytic)
 };
 
 // Task descriptor (16 bytes), produced by the plan kernel, consumed by the persistent kernel.
@@ -107,9 +108,12 @@ __host__ __device__ inline void split_range(int ns, int S, int sl, int& ks0, int
 // Token-tile cap of an expert's m-tiles: dual gate/up tiles of up to MXM_DUAL_TILE tokens fit one TMEM
 // accumulator buffer (2 x 160 columns next to a 3-slot A ring); register-accumulated tiles (g128 W-A dual, or gate and up as two sub-loops) keep
 // 64 columns per warpgroup half in registers -> 64 tokens.
+#ifndef MXM_REG_TILE
+#define MXM_REG_TILE 64  // token-tile cap of register-accumulated (g128 W-A / two-sub-loop) m-tiles
+#endif
 __host__ __device__ inline int tile_cap(const ExpertDesc& e) {
   const bool reg = !e.dual || (kind_is_wa(e.blk[0].geo.kind) && e.blk[0].geo.group == 128);
-  return reg ? 64 : MXM_DUAL_TILE;
+  return reg ? MXM_REG_TILE : MXM_DUAL_TILE;
 }
 // Down tasks pair two 128-channel output tiles (two mats sharing the h tile) unless the down is a g128
 // W-A block whose register-accumulated drain would exceed 64 columns per thread.

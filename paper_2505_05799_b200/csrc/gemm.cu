@@ -429,28 +429,39 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
   constexpr int NCH = HALF / CH;
   constexpr float kMagic = 12582912.f;  // 2^23 + 2^22
   if constexpr (I8 && F8) {
-    // per 8-column chunk: both mats' TMEM loads and the chunk's factors (a, b: broadcast float4s) in flight
-    // together, one wait, then 2 FFMA2 per element pair (no cross-chunk software pipelining: at 128
+    // per chunk of FCH columns: both mats' TMEM loads and the chunk's factors (a, b: broadcast float4s) in
+    // flight together, one wait, then 2 FFMA2 per element pair (no cross-chunk software pipelining: at 128
     // registers ptxas serialises it anyway, and one round trip per chunk is what that costs)
+#ifndef MXM_F8_CH
+#define MXM_F8_CH 8
+#endif
+    constexpr int FCH = (HALF % MXM_F8_CH == 0) ? MXM_F8_CH : 8;
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      const int c0 = c * CH;
-      uint32_t xa[CH], xb[CH];
+    for (int c = 0; c < HALF / FCH; ++c) {
+      const int c0 = c * FCH;
+      uint32_t xa[FCH], xb[FCH];
 #pragma unroll
-      for (int j = 0; j < CH; ++j) xb[j] = 0u;
-      tmem_ld8(addrA + c0, xa);
-      if constexpr (TWO) tmem_ld8(addrB + c0, xb);
-      const float4 a0 = *reinterpret_cast<const float4*>(sa + c0);
-      const float4 a1 = *reinterpret_cast<const float4*>(sa + c0 + 4);
-      const float4 b0 = *reinterpret_cast<const float4*>(sa + 128 + c0);
-      const float4 b1 = *reinterpret_cast<const float4*>(sa + 128 + c0 + 4);
-      tmem_ld_wait_regs(xa, xb);
-      const float2 ac[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
-                            make_float2(a1.z, a1.w)};
-      const float2 bc[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                            make_float2(b1.z, b1.w)};
+      for (int j = 0; j < FCH; ++j) xb[j] = 0u;
+      if constexpr (FCH == 16) {
+        tmem_ld16(addrA + c0, xa);
+        if constexpr (TWO) tmem_ld16(addrB + c0, xb);
+      } else {
+        tmem_ld8(addrA + c0, *reinterpret_cast<uint32_t(*)[8]>(xa));
+        if constexpr (TWO) tmem_ld8(addrB + c0, *reinterpret_cast<uint32_t(*)[8]>(xb));
+      }
+      float2 ac[FCH / 2], bc[FCH / 2];
 #pragma unroll
-      for (int j = 0; j < CH; j += 2) {
+      for (int q = 0; q < FCH / 4; ++q) {
+        const float4 a4 = *reinterpret_cast<const float4*>(sa + c0 + 4 * q);
+        const float4 b4 = *reinterpret_cast<const float4*>(sa + 128 + c0 + 4 * q);
+        ac[2 * q] = make_float2(a4.x, a4.y);
+        ac[2 * q + 1] = make_float2(a4.z, a4.w);
+        bc[2 * q] = make_float2(b4.x, b4.y);
+        bc[2 * q + 1] = make_float2(b4.z, b4.w);
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < FCH; j += 2) {
         const int col = c0 + j;
         const float2 fa = make_float2(__uint_as_float(xa[j]), __uint_as_float(xa[j + 1]));
         acc2[DST0 + col / 2] = ffma2(ffma2(fa, ac[j / 2], bc[j / 2]), make_float2(sw0, sw0), acc2[DST0 + col / 2]);

@@ -48,12 +48,18 @@ __device__ int block_excl_scan(int v, int* warp_tot, int* out_total) {
   return base + x - v;
 }
 
+__device__ __forceinline__ int pow2_index(int nt) { return nt <= 16 ? 0 : (nt <= 32 ? 1 : (nt <= 64 ? 2 : 3)); }
+
 // token tile of an m-tile with m rows: 16 / 32 / 64 / MXM_DUAL_TILE (the TMA boxes, MMA N)
 __device__ __forceinline__ int pow2_tile(int m) {
   return m <= 16 ? 16 : (m <= 32 ? 32 : (m <= 64 ? 64 : MXM_DUAL_TILE));
 }
 
+// LPT key of one m-tile group: the measured cost (mxm_profile_tile_costs, "pre-profiled ... costs") when the
+// layer carries one, else an analytic estimate (MMA cycles at the kind's rate vs operand bytes over a per-SM feed)
 __device__ __forceinline__ float tile_cost(const ExpertDesc& e, int d, int nt) {
+  const int ni = pow2_index(nt);
+  if (e.cost[ni] > 0.f) return e.cost[ni] * 1e6f;  // ms -> ns-scale units; only the order matters
   const LinDesc& g = e.blk[0];
   const float rate = kind_is_wa(g.geo.kind) ? 8192.f : 4096.f;  // MAC / cycle / SM
   const float mma = 2.f * 128.f * (float)nt * (float)d / rate;

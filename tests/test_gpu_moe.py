@@ -145,3 +145,26 @@ def test_split_k_unequal_shared_inter(mx):
         e, layer, y = _parity(case)
         assert e <= TOL, (T, e)
         assert np.array_equal(gpu_run(layer, case), y)
+
+
+def test_tile_costs_profile_and_plan(mx):
+    """mxm_profile_tile_costs: positive per-(expert, token tile) costs, larger for bigger tiles and for
+    heavier schemes; feeding them to the planner changes only the task order, so y is bitwise unchanged."""
+    cfg = C.LayerConfig("costs", 4, 1, 256, 512, 512, 2, 200)
+    table = [[C.W16] * 3, [C.WO(2, 128)] * 3, [C.WA(8, -1)] * 3, [C.WA(4, 128)] * 3, [C.WO(4, 128)] * 3]
+    case = make_case(cfg, table, 200, seed=3)
+    layer = gpu_layer(case)
+    y0 = gpu_run(layer, case)
+    costs = layer.profile_tile_costs()
+    assert costs.shape == (5, 4) and np.isfinite(costs).all() and (costs > 0).all(), costs
+    for v in range(4):
+        assert costs[v, 3] >= 0.8 * costs[v, 0], (v, costs[v])  # a 96-token (or capped) tile is not cheaper
+    layer.set_tile_costs(costs)
+    y1 = gpu_run(layer, case)
+    assert np.array_equal(y0, y1)
+    n, ex = layer.task_stats(case["T"], case["k"])
+    assert n == ex > 0
+    e = row_rel_err(y1, oracle_run(oracle_layer(case), case))
+    assert e <= TOL, e
+    layer.set_tile_costs(None)
+    assert np.array_equal(gpu_run(layer, case), y0)
