@@ -12,7 +12,10 @@ constexpr int kNumSms = 148;
 #ifndef MXM_ASLOTS
 #define MXM_ASLOTS 2  // TMEM A-ring depth of the group-GEMM (gemm.cu); sets the dual token tile below
 #endif
-#define MXM_DUAL_TILE (MXM_ASLOTS == 3 ? 80 : 96)  // max tokens of a dual (gate|up or paired-down) m-tile
+#ifndef MXM_ACC_BUFS
+#define MXM_ACC_BUFS 2  // TMEM accumulator buffers (3: 64-token dual tiles, one more MMA/epilogue overlap stage)
+#endif
+#define MXM_DUAL_TILE (MXM_ACC_BUFS == 3 ? 64 : (MXM_ASLOTS == 3 ? 80 : 96))  // max tokens of a dual m-tile
 constexpr int kRowsPerTile = 128;  // output channels per tile (UMMA M)
 
 // Packed-format kinds (docs/packed_format.md)

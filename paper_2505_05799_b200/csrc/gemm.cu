@@ -36,7 +36,7 @@ namespace mxm {
 #define MXM_TILE_KB 16
 #endif
 #ifndef MXM_SSLOTS
-#define MXM_SSLOTS 4
+#define MXM_SSLOTS 8
 #endif
 constexpr int kStages = MXM_STAGES;
 constexpr int kRing = 4;
@@ -46,9 +46,9 @@ constexpr int kRing = 4;
 // 2 mats x 32 columns), decoupled from the 4 smem stages by its own ready / empty barriers.
 // MXM_ASLOTS=3 (2 x 160 accumulator columns, 80-token tiles, 3 A slots) was measured slower on every
 // config (DSV2 GEMM 0.93 -> 1.09 ms): the smaller tiles cost more than the deeper A ring saves.
-constexpr int kAccBufs = 2;
+constexpr int kAccBufs = MXM_ACC_BUFS;
 constexpr int kASlots = MXM_ASLOTS;
-constexpr int kAccCols = kASlots == 3 ? 160 : 192;  // 2 x 160 + 3 x 64 = 2 x 192 + 2 x 64 = 512 columns
+constexpr int kAccCols = kAccBufs == 3 ? 128 : (kASlots == 3 ? 160 : 192);  // 2x160+3x64 = 2x192+2x64 = 3x128+2x64
 constexpr int kMat1Col = kAccCols / 2;               // column offset of mat 1 inside an accumulator buffer
 constexpr int kTmemA = kAccBufs * kAccCols;
 static_assert(kTmemA + 64 * kASlots == 512, "TMEM partition");
@@ -65,13 +65,12 @@ constexpr int kCtlBytes = 8192;
 // array, from the 16-byte-aligned floor) next to the stage's operands; the epilogue drains the event's
 // accumulator against them, then releases the slot.
 constexpr int kSSlots = MXM_SSLOTS;
-// [0,256) mat-0 s_w | [256,512) mat-1 s_w | [512,1024) s_a (<= 125 floats) | [1024,1536) code sums (w4a4),
-// all as bulk-copied (s_a / sums from the 16-B aligned floor of the m-tile's span) | [1536,2048) per token column
-// drain factor a (s_a, or s_a 2^18 for w4a4) | [2048,2560) w4a4 offset correction b = -8 s_a sum(q_a): written,
-// 16-B aligned from column 0, once the bulk copies landed, by the scale-staging warps (sready), so the epilogue reads
-// them as broadcast float4s with no per-warp restaging on its critical path (scale-staging warps 2-3)
-constexpr int kSSlotBytes = 2560;
-constexpr int kSlotA = 1536, kSlotB = 2048;
+// scale slot of one g128 drain event, written by the staging warp (stage_scales) from global memory: [0,256) mat-0
+// s_w | [256,512) mat-1 s_w (bf16 per channel) | [512,1024) per token column drain factor a (s_a, or s_a 2^18 for
+// w4a4) | [1024,1536) w4a4 offset correction b = -8 s_a sum(q_a); 16-B aligned from column 0 so the epilogue reads
+// the factors as broadcast float4s
+constexpr int kSSlotBytes = 1536;
+constexpr int kSlotA = 512, kSlotB = 1024;
 constexpr int kOffScale = kOffCtl + kCtlBytes;
 constexpr int kSmemBytes = kOffScale + kSSlots * kSSlotBytes + 1024;
 
@@ -171,7 +170,7 @@ __device__ __forceinline__ bool bf2_nonfinite(uint32_t v) {
 #ifdef MXM_TRACE
 // per-stage event timestamps of CTA 0 (diagnostic build): [event][index], see tools/diag_trace.py
 constexpr int kTrN = 2048;
-__device__ unsigned long long g_tr[12][kTrN];
+__device__ unsigned long long g_tr[13][kTrN];
 #define TR(ev, idx) do { if (blockIdx.x == 0 && (idx) < kTrN) g_tr[ev][idx] = clock64(); } while (0)
 #else
 #define TR(ev, idx) do { } while (0)
@@ -428,6 +427,72 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
   constexpr int CH = 8;  // 16-wide staging + 64 accumulators exceeds the 128-register epilogue budget (spills)
   constexpr int NCH = HALF / CH;
   constexpr float kMagic = 12582912.f;  // 2^23 + 2^22
+#ifdef MXM_F8_MATWISE
+  if constexpr (I8 && F8 && HALF == 32) {
+    // mat by mat: all 32 columns of a mat in one TMEM load (one round trip per mat), factors as broadcast float4s
+#pragma unroll
+    for (int m = 0; m < (TWO ? 2 : 1); ++m) {
+      uint32_t xv[32];
+      tmem_ld32(m == 0 ? addrA : addrB, xv);
+      const float2 swm = m == 0 ? make_float2(sw0, sw0) : make_float2(sw1, sw1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 a4 = *reinterpret_cast<const float4*>(sa + 4 * q);
+        const float4 b4 = *reinterpret_cast<const float4*>(sa + 128 + 4 * q);
+        const int dst = (m == 0 ? DST0 : 16) + 2 * q;
+        acc2[dst] = ffma2(ffma2(make_float2(__uint_as_float(xv[4 * q]), __uint_as_float(xv[4 * q + 1])),
+                                make_float2(a4.x, a4.y), make_float2(b4.x, b4.y)), swm, acc2[dst]);
+        acc2[dst + 1] = ffma2(ffma2(make_float2(__uint_as_float(xv[4 * q + 2]), __uint_as_float(xv[4 * q + 3])),
+                                    make_float2(a4.z, a4.w), make_float2(b4.z, b4.w)), swm, acc2[dst + 1]);
+      }
+    }
+    return;
+  }
+#endif
+#ifdef MXM_F8_2CH
+  if constexpr (I8 && F8 && HALF % 16 == 0) {
+    // two 8-column chunks per round trip: both chunks' TMEM loads (both mats) issued together
+#pragma unroll
+    for (int c = 0; c < HALF / 16; ++c) {
+      const int c0 = c * 16;
+      uint32_t xa[2][8], xb[2][8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) xb[0][j] = xb[1][j] = 0u;
+      tmem_ld8(addrA + c0, xa[0]);
+      tmem_ld8(addrA + c0 + 8, xa[1]);
+      if constexpr (TWO) {
+        tmem_ld8(addrB + c0, xb[0]);
+        tmem_ld8(addrB + c0 + 8, xb[1]);
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float4 a4 = *reinterpret_cast<const float4*>(sa + c0 + 8 * h + 4 * q);
+          const float4 b4 = *reinterpret_cast<const float4*>(sa + 128 + c0 + 8 * h + 4 * q);
+          const int dst = (c0 + 8 * h + 4 * q) / 2;
+          const float2 a01 = make_float2(a4.x, a4.y), a23 = make_float2(a4.z, a4.w);
+          const float2 b01 = make_float2(b4.x, b4.y), b23 = make_float2(b4.z, b4.w);
+          acc2[DST0 + dst] = ffma2(ffma2(make_float2(__uint_as_float(xa[h][4 * q]), __uint_as_float(xa[h][4 * q + 1])),
+                                         a01, b01), make_float2(sw0, sw0), acc2[DST0 + dst]);
+          acc2[DST0 + dst + 1] = ffma2(ffma2(make_float2(__uint_as_float(xa[h][4 * q + 2]),
+                                                         __uint_as_float(xa[h][4 * q + 3])), a23, b23),
+                                       make_float2(sw0, sw0), acc2[DST0 + dst + 1]);
+          if constexpr (TWO) {
+            acc2[16 + dst] = ffma2(ffma2(make_float2(__uint_as_float(xb[h][4 * q]), __uint_as_float(xb[h][4 * q + 1])),
+                                         a01, b01), make_float2(sw1, sw1), acc2[16 + dst]);
+            acc2[16 + dst + 1] = ffma2(ffma2(make_float2(__uint_as_float(xb[h][4 * q + 2]),
+                                                         __uint_as_float(xb[h][4 * q + 3])), a23, b23),
+                                       make_float2(sw1, sw1), acc2[16 + dst + 1]);
+          }
+        }
+      }
+    }
+    return;
+  }
+#endif
   if constexpr (I8 && F8) {
     // per chunk of FCH columns: both mats' TMEM loads and the chunk's factors (a, b: broadcast float4s) in
     // flight together, one wait, then 2 FFMA2 per element pair (no cross-chunk software pipelining: at 128
@@ -714,6 +779,7 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned l
 
 struct MmaState {
   uint32_t stage, sphase, abuf, acc_ph, aidx;  // aidx: TS stages so far (A slot = aidx % kASlots)
+  int nev;                                      // drain events committed (trace index, diagnostic build)
   int ntr;                                      // stages issued (trace index, diagnostic build)
 };
 
@@ -747,9 +813,11 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
     const bool ev_start = g128 || ks == 0, ev_end = g128 || ks == ns - 1;
     if (ev_start) {
       b0 = st.abuf;
+      if ((threadIdx.x & 31) == 0) TR(10, st.nev);
       twait(&ctl.acce[b0], ((st.acc_ph >> b0) & 1) ^ 1, pc[4], prof_on);
+      if ((threadIdx.x & 31) == 0) TR(11, st.nev);
       st.acc_ph ^= 1u << b0;
-      st.abuf = (st.abuf + 1) & (kAccBufs - 1);
+      st.abuf = st.abuf + 1 == kAccBufs ? 0 : st.abuf + 1;
     }
     const uint32_t stage = st.stage;
     const uint32_t d0 = tmem + b0 * (uint32_t)kAccCols;
@@ -805,6 +873,10 @@ __device__ __forceinline__ void mma_subloop(Ctl& ctl, uint8_t* smem, uint32_t tm
       if (any_ts) mma_commit(&ctl.aempty[aslot]);
       if (ev_end) mma_commit(&ctl.accf[b0]);
     }
+    if (ev_end) {
+      if ((threadIdx.x & 31) == 0) TR(12, st.nev);  // (trace build: event-indexed commit time)
+      ++st.nev;
+    }
     __syncwarp();
     if (prof_on) {
       pc[11] += clock64() - t_iss;
@@ -838,6 +910,145 @@ __device__ __forceinline__ void mma_subloop_mode(Ctl& ctl, uint8_t* smem, uint32
 // ---------------------------------------------------------------- the kernel
 // SPLIT: the launch may cut downs into K-slices (tiny T, workspace has the partial buffer). A separate
 // instantiation, so the split-K bookkeeping costs the large-T kernel no registers.
+// The per-stage copies of one task's sub-loops, split over two warps because each cp.async.bulk / TMA issue
+// occupies its warp for ~100-190 cycles (tools/copy_issue.cu): ROLE 0 (producer, warp 0): the stage's
+// expect_tx and mat 0's packed chunk (+ its copied group meta); ROLE 1 (warp 2): the dependency wait of
+// phase-2 tasks, mat 1's chunk and the token tile (TMA). Both walk the same stage / parity sequence and wait
+// for the same `empty` phase; a copy may land before the expect_tx (the transaction count may go negative).
+#ifndef MXM_HELPER_SLEEP
+#define MXM_HELPER_SLEEP 0
+#endif
+template <int ROLE, bool SPLIT>
+__device__ __forceinline__ void copy_task(const GemmParams& p, const Task& t, Ctl& ctl, uint8_t* smem,
+                                          uint32_t& stage, uint32_t& sphase, int n_split,
+                                          unsigned long long (&pc)[16], bool prof_on, int& n_tr_p) {
+  if (ROLE == 1 && t.phase == 2) {
+    const ExpertDesc& e = p.ex[t.expert];
+    // per-token W-A downs wait for the h-quant pass; all others only for the gate/up tiles
+    const bool wa_pt = kind_is_wa(e.blk[2].geo.kind) && e.blk[2].geo.group != 128;
+    const int* ctr = (wa_pt ? p.hq_done : p.p1_done) + t.gid;
+    const int need = wa_pt ? p.grp_nq[t.gid] : p.grp_n1[t.gid];
+    const unsigned long long td = prof_on ? clock64() : 0ull;
+    while (ld_acquire_gpu(ctr) < need) __nanosleep(64);
+    if (prof_on) pc[2] += clock64() - td;
+    fence_proxy_async_global();
+  }
+  SubLoop sl[2];
+  const int nsl = build_subloops(t, p.ex, p.d, n_split, sl);
+  const int nti = nt_index(t.nt);
+  for (int si = 0; si < nsl; ++si) {
+    const SubLoop s = sl[si];
+    const CUtensorMap* map = &p.tmap[s.bmap][nti];
+    // per-mat chunk streams (gate and up may differ in bits / group / format)
+    const PackGeom& g0 = s.mat[0]->geo;
+    const PackGeom& g1 = s.mat[s.nmats - 1]->geo;
+    const uint32_t cb0 = (uint32_t)g0.code_bytes, mb0 = (uint32_t)g0.meta_bytes;
+    const uint32_t cb1 = (uint32_t)g1.code_bytes, mb1 = (uint32_t)g1.meta_bytes;
+    const int gst0 = g0.group / g0.ks, gst1 = g1.group / g1.ks;
+    const int ksb = SPLIT ? s.ks0 : 0, kse = SPLIT ? s.ks1 : s.ns;
+    const uint8_t* src0 = s.mat[0]->packed + (SPLIT ? chunk_offset(g0, s.tile[0], ksb) : (int64_t)s.tile[0] * g0.rb_bytes);
+    const uint8_t* src1 = s.nmats == 2 ? s.mat[1]->packed + (SPLIT ? chunk_offset(g1, s.tile[1], ksb)
+                                                                      : (int64_t)s.tile[1] * g1.rb_bytes)
+                                       : nullptr;
+    const int kstep = s.i8 ? 128 : 64;
+    int gc0 = SPLIT ? ksb % gst0 : 0, gc1 = SPLIT ? ksb % gst1 : 0;
+    // a split-K slice that starts inside a weight-only group: its first stage is laid out as a group
+    // start, [group meta (copied from the group-start chunk) | codes], so the transform needs no case
+    const uint8_t* gm0 = (SPLIT && gc0 != 0 && g0.kind == KIND_WO)
+                             ? s.mat[0]->packed + chunk_offset(g0, s.tile[0], ksb - gc0) : nullptr;
+    const uint8_t* gm1 = (SPLIT && src1 && gc1 != 0 && g1.kind == KIND_WO)
+                             ? s.mat[1]->packed + chunk_offset(g1, s.tile[1], ksb - gc1) : nullptr;
+    for (int ks = ksb; ks < kse; ++ks) {
+      const uint32_t c0 = cb0 + (gc0 == 0 ? mb0 : 0u);
+      const uint32_t c1 = src1 ? cb1 + (gc1 == 0 ? mb1 : 0u) : 0u;
+      const uint32_t e0 = SPLIT && gm0 ? mb0 : 0u, e1 = SPLIT && gm1 ? mb1 : 0u;
+      if (++gc0 == gst0) gc0 = 0;
+      if (++gc1 == gst1) gc1 = 0;
+      if (ROLE == 1) {  // off the transform warps' issue slots: poll with a short sleep (4 stages of slack)
+        while (!mbar_try_wait(&ctl.empty[stage], sphase ^ 1))
+          if (MXM_HELPER_SLEEP) __nanosleep(MXM_HELPER_SLEEP);
+      } else {
+        twait(&ctl.empty[stage], sphase ^ 1, pc[1], prof_on);
+      }
+      uint8_t* slot = smem + stage * kSlotBytes;
+#ifndef MXM_COPY_SPLIT
+#define MXM_COPY_SPLIT 2  // 1: warp 2 issues mat 1 + token tile; 2 (measured best): warp 2 issues only the token tile
+#endif
+      const bool mat1_here = (ROLE == 0) == (MXM_COPY_SPLIT == 2);
+      if (ROLE == 0) {
+        TR(0, n_tr_p);
+        mbar_arrive_expect_tx(&ctl.full[stage], (uint32_t)t.nt * 128u + c0 + c1 + e0 + e1);
+        if (e0) bulk_load(slot + kTileBytes, gm0, e0, &ctl.full[stage]);
+        bulk_load(slot + kTileBytes + e0, src0, c0, &ctl.full[stage]);
+        ++n_tr_p;
+      }
+      if (src1 && mat1_here) {
+        if (e1) bulk_load(slot + 2 * kTileBytes, gm1, e1, &ctl.full[stage]);
+        bulk_load(slot + 2 * kTileBytes + e1, src1, c1, &ctl.full[stage]);
+      }
+      if (ROLE == 1) tma_load_2d(slot, map, &ctl.full[stage], ks * kstep, t.row0);
+      src0 += c0;
+      gm0 = nullptr;
+      if (src1) {
+        src1 += c1;
+        gm1 = nullptr;
+      }
+      if (++stage == kStages) {
+        stage = 0;
+        sphase ^= 1;
+      }
+    }
+  }
+}
+
+// Scale staging for one weight-activation g128 sub-loop (warp 3): per 128-K group, once the epilogue released the
+// scale slot (sempty), the drain factors of the group -- per channel s_w of each mat, per token column
+// a = s_a (s_a 2^18 for w4a4) and b = -8 s_a sum(q_a) -- read straight from global memory (no bulk copies on the
+// producer's path) and written 16-B aligned into the slot, then sready.
+__device__ __forceinline__ void stage_scales(const GemmParams& p, const Task& t, const SubLoop& s, Ctl& ctl,
+                                             uint8_t* smem, uint32_t& xsidx, int lane, unsigned long long (&pc)[16],
+                                             bool prof_on) {
+  const float* xs_t = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;
+  const int32_t* xc_t = (t.phase == 0) ? p.xc[s.mat[0]->in_slot] : p.Hc;
+  const uint16_t* w0 = reinterpret_cast<const uint16_t*>(s.mat[0]->packed + s.mat[0]->geo.wa_scale_off) +
+                       s.tile[0] * 128;
+  const uint16_t* w1 = s.nmats == 2 ? reinterpret_cast<const uint16_t*>(s.mat[1]->packed + s.mat[1]->geo.wa_scale_off) +
+                                          s.tile[1] * 128
+                                    : nullptr;
+  for (int ks = 0; ks < s.ns; ++ks) {
+    // this group's values (loads in flight before the slot wait)
+    const uint2 sw0 = *reinterpret_cast<const uint2*>(w0 + (int64_t)ks * s.mat[0]->geo.N + 4 * lane);
+    const uint2 sw1 = w1 ? *reinterpret_cast<const uint2*>(w1 + (int64_t)ks * s.mat[1]->geo.N + 4 * lane)
+                         : make_uint2(0, 0);
+    float sa[3] = {0.f, 0.f, 0.f};
+    int qs[3] = {0, 0, 0};
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const int c = lane + 32 * h;
+      if (c < t.rows) {
+        sa[h] = __ldcg(xs_t + (int64_t)ks * p.hs_stride + t.row0 + c);
+        if (s.f8) qs[h] = __ldcg(xc_t + (int64_t)ks * p.hs_stride + t.row0 + c);
+      }
+    }
+    const uint32_t ss = xsidx & (kSSlots - 1);
+    twait(&ctl.sempty[ss], ((xsidx / kSSlots) & 1) ^ 1, pc[8], prof_on);
+    uint8_t* slotp = smem + kOffScale + ss * kSSlotBytes;
+    reinterpret_cast<uint2*>(slotp)[lane] = sw0;
+    reinterpret_cast<uint2*>(slotp + 256)[lane] = sw1;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const int c = lane + 32 * h;
+      if (c < (int)t.nt) {
+        reinterpret_cast<float*>(slotp + kSlotA)[c] = s.f8 ? sa[h] * 262144.f : sa[h];
+        reinterpret_cast<float*>(slotp + kSlotB)[c] = s.f8 ? __fmul_rn(-8.f * (float)qs[h], sa[h]) : 0.f;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ctl.sready[ss]);
+    ++xsidx;
+  }
+}
+
 // DUMP: test-only instantiation that also copies every weight-activation accumulator to p.dump (and the bf16 h
 // of fused-quantized downs to p.H) for the bit-exact accumulator tests; never launched by mxm_moe_group_gemm.
 template <bool SPLIT, bool DUMP>
@@ -868,7 +1079,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(&ctl.sfull[i], 1);
       mbar_init(&ctl.sempty[i], 8);  // the 8 epilogue warps
-      mbar_init(&ctl.sready[i], 2);  // the scale-staging warps 2-3 (drain factors staged)
+      mbar_init(&ctl.sready[i], 1);  // the scale-staging warp 3 (drain factors staged)
     }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&ctl.accf[i], 1);
@@ -919,9 +1130,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   if (warp == 0) {
     // =========================== producer
     if (lane == 0) {
-      uint32_t stage = 0, sphase = 0, sidx = 0;
+      uint32_t stage = 0, sphase = 0;
       int n_tr_p = 0;
-      (void)n_tr_p;
       for (uint32_t it = 0;; ++it) {
         const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
         const int idx = atomicAdd(&p.meta[5], 1);
@@ -936,95 +1146,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         mbar_arrive(&ctl.tfull[slot]);
         if (t.phase == 255) break;
         if (t.phase == 1) continue;
-        if (t.phase == 2) {
-          const ExpertDesc& e = p.ex[t.expert];
-          // per-token W-A downs wait for the h-quant pass; all others only for the gate/up tiles
-          const bool wa_pt = kind_is_wa(e.blk[2].geo.kind) && e.blk[2].geo.group != 128;
-          const int* ctr = (wa_pt ? p.hq_done : p.p1_done) + t.gid;
-          const int need = wa_pt ? p.grp_nq[t.gid] : p.grp_n1[t.gid];
-          const unsigned long long td = prof_on ? clock64() : 0ull;
-          while (ld_acquire_gpu(ctr) < need) __nanosleep(64);
-          if (prof_on) pc[2] += clock64() - td;
-          fence_proxy_async_global();
-        }
-        SubLoop sl[2];
-        const int nsl = build_subloops(t, p.ex, p.d, n_split, sl);
-        const int nti = nt_index(t.nt);
-        for (int si = 0; si < nsl; ++si) {
-          const SubLoop s = sl[si];
-          const CUtensorMap* map = &p.tmap[s.bmap][nti];
-          // per-mat chunk streams (gate and up may differ in bits / group / format)
-          const PackGeom& g0 = s.mat[0]->geo;
-          const PackGeom& g1 = s.mat[s.nmats - 1]->geo;
-          const uint32_t cb0 = (uint32_t)g0.code_bytes, mb0 = (uint32_t)g0.meta_bytes;
-          const uint32_t cb1 = (uint32_t)g1.code_bytes, mb1 = (uint32_t)g1.meta_bytes;
-          const int gst0 = g0.group / g0.ks, gst1 = g1.group / g1.ks;
-          const int ksb = SPLIT ? s.ks0 : 0, kse = SPLIT ? s.ks1 : s.ns;
-          const uint8_t* src0 = s.mat[0]->packed + (SPLIT ? chunk_offset(g0, s.tile[0], ksb) : (int64_t)s.tile[0] * g0.rb_bytes);
-          const uint8_t* src1 = s.nmats == 2 ? s.mat[1]->packed + (SPLIT ? chunk_offset(g1, s.tile[1], ksb)
-                                                                            : (int64_t)s.tile[1] * g1.rb_bytes)
-                                             : nullptr;
-          uint8_t* const dst0 = tileX(0, 0);
-          uint8_t* const dst1 = tileX(0, 1);
-          const int str0 = kSlotBytes, str1 = kSlotBytes;
-          const int kstep = s.i8 ? 128 : 64;
-          int gc0 = SPLIT ? ksb % gst0 : 0, gc1 = SPLIT ? ksb % gst1 : 0;
-          // a split-K slice that starts inside a weight-only group: its first stage is laid out as a group
-          // start, [group meta (copied from the group-start chunk) | codes], so the transform needs no case
-          const uint8_t* gm0 = (SPLIT && gc0 != 0 && g0.kind == KIND_WO)
-                                   ? s.mat[0]->packed + chunk_offset(g0, s.tile[0], ksb - gc0) : nullptr;
-          const uint8_t* gm1 = (SPLIT && src1 && gc1 != 0 && g1.kind == KIND_WO)
-                                   ? s.mat[1]->packed + chunk_offset(g1, s.tile[1], ksb - gc1) : nullptr;
-          for (int ks = ksb; ks < kse; ++ks) {
-            const uint32_t c0 = cb0 + (gc0 == 0 ? mb0 : 0u);
-            const uint32_t c1 = src1 ? cb1 + (gc1 == 0 ? mb1 : 0u) : 0u;
-            const uint32_t e0 = SPLIT && gm0 ? mb0 : 0u, e1 = SPLIT && gm1 ? mb1 : 0u;
-            if (++gc0 == gst0) gc0 = 0;
-            if (++gc1 == gst1) gc1 = 0;
-            twait(&ctl.empty[stage], sphase ^ 1, pc[1], prof_on);
-            TR(0, n_tr_p);
-            ++n_tr_p;
-            mbar_arrive_expect_tx(&ctl.full[stage], (uint32_t)t.nt * 128u + c0 + c1 + e0 + e1);
-            if (e0) bulk_load(dst0 + stage * str0, gm0, e0, &ctl.full[stage]);
-            bulk_load(dst0 + stage * str0 + e0, src0, c0, &ctl.full[stage]);
-            src0 += c0;
-            gm0 = nullptr;
-            if (src1) {
-              if (e1) bulk_load(dst1 + stage * str1, gm1, e1, &ctl.full[stage]);
-              bulk_load(dst1 + stage * str1 + e1, src1, c1, &ctl.full[stage]);
-              src1 += c1;
-              gm1 = nullptr;
-            }
-            tma_load_2d(tileB(stage), map, &ctl.full[stage], ks * kstep, t.row0);
-            if (s.g128) {  // the 128-K group's scales into the scale ring (read by the epilogue)
-              const uint32_t ss = sidx & (kSSlots - 1);
-              twait(&ctl.sempty[ss], ((sidx / kSSlots) & 1) ^ 1, pc[1], prof_on);
-              uint8_t* dst = smem + kOffScale + ss * kSSlotBytes;
-              const float* abase = t.phase == 0 ? p.xs[s.mat[0]->in_slot] : p.Hs;
-              uint32_t aoff;
-              const float* asrc = ascale_span(abase, p.hs_stride, ks, t.row0, aoff);
-              const uint32_t abytes = ((aoff + t.nt) * 4u + 15u) & ~15u;
-              const uint32_t wbytes = 256u * (uint32_t)s.nmats;
-              mbar_arrive_expect_tx(&ctl.sfull[ss], wbytes + abytes * (s.f8 ? 2u : 1u));
-              if (s.f8) {  // the group's activation code sums (same group-major layout and alignment as s_a)
-                const int32_t* cbase = t.phase == 0 ? p.xc[s.mat[0]->in_slot] : p.Hc;
-                bulk_load(dst + 1024, cbase + (int64_t)ks * p.hs_stride + t.row0 - aoff, abytes, &ctl.sfull[ss]);
-              }
-              const uint8_t* w0 = s.mat[0]->packed + g0.wa_scale_off + ((int64_t)ks * g0.N + s.tile[0] * 128) * 2;
-              bulk_load(dst, w0, 256u, &ctl.sfull[ss]);
-              if (s.nmats == 2) {
-                const uint8_t* w1 = s.mat[1]->packed + g1.wa_scale_off + ((int64_t)ks * g1.N + s.tile[1] * 128) * 2;
-                bulk_load(dst + 256, w1, 256u, &ctl.sfull[ss]);
-              }
-              bulk_load(dst + 512, asrc, abytes, &ctl.sfull[ss]);
-              ++sidx;
-            }
-            if (++stage == kStages) {
-              stage = 0;
-              sphase ^= 1;
-            }
-          }
-        }
+        copy_task<0, SPLIT>(p, t, ctl, smem, stage, sphase, n_split, pc, prof_on, n_tr_p);
       }
     }
     __syncwarp();
@@ -1034,7 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     uint32_t stage = 0, sphase = 0, abuf = 0;
     uint32_t acc_ph = 0;  // bit b: parity of the next wait on acce[b] (phase bits, no local arrays)
     uint32_t aidx = 0;    // TS stages issued so far (A-ring slot and parity)
-    int ntr_m = 0;
+    int ntr_m = 0, nev_m = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
       twait(&ctl.tfull[slot], rphase, pc[3], prof_on);
@@ -1052,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         const uint32_t ns = bcast((uint32_t)(SPLIT ? s.ks1 - s.ks0 : s.ns)), g128 = bcast((uint32_t)s.g128);
         const uint32_t xf = bcast((uint32_t)s.xform);
         const uint32_t i8 = bcast((uint32_t)s.i8), f8 = bcast((uint32_t)s.f8), two = bcast((uint32_t)(s.nmats == 2));
-        MmaState st{stage, sphase, abuf, acc_ph, aidx, ntr_m};
+        MmaState st{stage, sphase, abuf, acc_ph, aidx, nev_m, ntr_m};
 #if defined(MXM_PROF_SUBLOOP) && defined(MXM_DEBUG_COUNTERS)
         const unsigned long long t_sl = prof_on ? clock64() : 0ull;
 #endif
@@ -1080,16 +1202,16 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         abuf = st.abuf;
         acc_ph = st.acc_ph;
         aidx = st.aidx;
+        nev_m = st.nev;
         ntr_m = st.ntr;
       }
     }
     __syncwarp();
   } else {
-    // =========================== scale staging (warps 2-3): per 128-K group of a g128 W-A sub-loop, once its
-    // scale slot landed (sfull), write the drain factors of every token column 16-B aligned into the slot
-    // (a = s_a, or s_a 2^18 for w4a4; b = -8 s_a sum(q_a)) and signal the epilogue (sready)
-    uint32_t xsidx = 0;
-    const int c0 = (warp - 2) * 32 + lane;  // this thread's token columns: c0 and c0 + 64
+    // =========================== warp 2: second copy issuer (mat 1 + token tile, copy_task ROLE 1);
+    // warp 3: scale staging of weight-activation g128 groups (stage_scales)
+    uint32_t stage = 0, sphase = 0, xsidx = 0;
+    int n_tr_h = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
       twait(&ctl.tfull[slot], rphase, pc[7], prof_on);
@@ -1098,37 +1220,24 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       if (lane == 0) mbar_arrive(&ctl.tempty[slot]);
       if (t.phase == 255) break;
       if (t.phase == 1) continue;
+      if (warp == 2) {
+        if (lane == 0) copy_task<1, SPLIT>(p, t, ctl, smem, stage, sphase, n_split, pc, prof_on, n_tr_h);
+        __syncwarp();
+        continue;
+      }
       SubLoop sl[2];
       const int nsl = build_subloops(t, p.ex, p.d, n_split, sl);
-      for (int si = 0; si < nsl; ++si) {
-        const SubLoop& s = sl[si];
-        if (!s.g128) continue;
-        const float* xs_t = (t.phase == 0) ? p.xs[s.mat[0]->in_slot] : p.Hs;
-        for (int ks = 0; ks < s.ns; ++ks) {
-          const uint32_t ss = xsidx & (kSSlots - 1);
-          twait(&ctl.sfull[ss], (xsidx / kSSlots) & 1, pc[8], prof_on);
-          uint8_t* slotp = smem + kOffScale + ss * kSSlotBytes;
-          uint32_t aoff;
-          (void)ascale_span(xs_t, p.hs_stride, ks, t.row0, aoff);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = c0 + 64 * h;
-            if (c < (int)t.nt) {
-              const float sav = reinterpret_cast<const float*>(slotp + 512)[aoff + c];
-              float av = sav, bv = 0.f;
-              if (s.f8) {
-                av = sav * 262144.f;
-                bv = __fmul_rn(-8.f * (float)reinterpret_cast<const int32_t*>(slotp + 1024)[aoff + c], sav);
-              }
-              reinterpret_cast<float*>(slotp + kSlotA)[c] = av;
-              reinterpret_cast<float*>(slotp + kSlotB)[c] = bv;
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl.sready[ss]);
-          ++xsidx;
+      bool any_g128 = false;
+      for (int si = 0; si < nsl; ++si) any_g128 |= sl[si].g128 != 0;
+      if (!any_g128) continue;
+      if (t.phase == 2) {  // h scales / sums come from this kernel's gate/up epilogues of the m-tile
+        if (lane == 0) {
+          while (ld_acquire_gpu(p.p1_done + t.gid) < p.grp_n1[t.gid]) __nanosleep(64);
         }
+        __syncwarp();
       }
+      for (int si = 0; si < nsl; ++si)
+        if (sl[si].g128) stage_scales(p, t, sl[si], ctl, smem, xsidx, lane, pc, prof_on);
     }
     __syncwarp();
   }
@@ -1340,7 +1449,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           }
         }
         const uint32_t b0 = abuf;
-        abuf = (abuf + 1) & (kAccBufs - 1);
+        abuf = abuf + 1 == kAccBufs ? 0 : abuf + 1;
         twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
         if (threadIdx.x == 256) TR(5, n_tr_e);
         acc_ph ^= 1u << b0;
@@ -1549,7 +1658,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           for (int ev = 0; ev < nev; ++ev) {
             float sw0 = nsw0, sw1 = nsw1;
             const uint32_t b0 = abuf;
-            abuf = (abuf + 1) & (kAccBufs - 1);
+            abuf = abuf + 1 == kAccBufs ? 0 : abuf + 1;
             twait(&ctl.accf[b0], (acc_ph >> b0) & 1, pc[10], prof_on);
             if (threadIdx.x == 256) TR(5, n_tr_e);
             acc_ph ^= 1u << b0;
@@ -1559,7 +1668,9 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             if (s.g128) {  // g128 event: the group's scales arrived in the scale ring with the stage
               ss = sidx & (kSSlots - 1);
               twait(&ctl.sready[ss], (sidx / kSSlots) & 1, pc[10], prof_on);  // factors staged by the transform
+#ifndef MXM_TRACE_PRODUCER
               if (threadIdx.x == 256) TR(7, n_tr_e);
+#endif
               const uint8_t* slotp = smem + kOffScale + ss * kSSlotBytes;
               sw0 = bf16f(reinterpret_cast<const uint16_t*>(slotp)[l]);
               if (two) sw1 = bf16f(reinterpret_cast<const uint16_t*>(slotp + 256)[l]);
@@ -1600,14 +1711,18 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               }
             }
 #ifndef MXM_ABL_EPI
+#ifndef MXM_TRACE_PRODUCER
             if (threadIdx.x == 256) TR(8, n_tr_e);
+#endif
             const unsigned long long t_dr = prof_on ? clock64() : 0ull;
             if (dst_hi)
               drain_event_any<16>(half, acc2, aA, aB, s.i8, s.f8, false, s.g128, sw0, sw1, sa_ev);
             else
               drain_event_any<0>(half, acc2, aA, aB, s.i8, s.f8, two, s.g128, sw0, sw1, sa_ev);
             if (prof_on) pc[12] += clock64() - t_dr;  // register-accumulating drain time (diagnostic build)
+#ifndef MXM_TRACE_PRODUCER
             if (threadIdx.x == 256) TR(9, n_tr_e);
+#endif
 #endif
             tc_fence_before();
             __syncwarp();

@@ -22,9 +22,9 @@ sw = torch.from_numpy(bench.gen_shared_weights(T, cfg.n_shared)).cuda() if cfg.n
 for _ in range(3): L(x, ids, w, sw)
 torch.cuda.synchronize()
 lib = ctypes.CDLL(os.environ["MXM_LIB"])
-buf = (ctypes.c_ulonglong * (12 * 2048))()
+buf = (ctypes.c_ulonglong * (13 * 2048))()
 lib.mxm_debug_trace(buf)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(12, 2048).astype(np.int64)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(13, 2048).astype(np.int64)
 n = int(min((a[3] > 0).sum(), (a[1] > 0).sum(), 1500))
 t0 = a[0, 0]
 print(f"{cfg.name} {tb}: first {n} stages of CTA 0 (cycles relative to the first load)")
@@ -53,3 +53,19 @@ if len(sys.argv) > 4 and sys.argv[4] == "full":
     for i in range(700, 716):
         r = a[:, i] - b[0]
         print(f"{i:4d} {r[0]:7d} {r[1]:7d} {r[2]:7d} {r[3]:7d} {r[4]:7d} {r[5]:7d} {r[7]:7d} {r[8]:7d} {r[9]:7d} {r[6]:7d}")
+
+nm = int(min((a[12] > 0).sum(), (a[5] > 0).sum(), (a[10] > 0).sum(), 1500))
+if nm > 20:
+    ev = np.arange(200, min(nm, 1400))
+    commit, has, done = a[12, ev], a[5, ev], a[6, ev]
+    wait_s, wait_e = a[10, ev + 2], a[11, ev + 2]  # MMA of event e+2 waits for the drain of event e (same buffer)
+    print("event-indexed (median over events 200..): MMA commit -> epilogue has %.0f | epilogue has -> done %.0f |"
+          " done -> MMA(e+2) wait end %.0f | MMA(e+2) wait %.0f | event period %.0f" % (
+          np.median(has - commit), np.median(done - has), np.median(wait_e - done), np.median(wait_e - wait_s),
+          np.median(np.diff(a[12, ev]))))
+
+if os.environ.get("TRACE_PRODUCER"):
+    ev = np.arange(200, 1400)
+    print("producer (median): stage start -> empty passed %.0f | empty -> before scale wait %.0f | sempty wait %.0f |"
+          " stage period %.0f" % (np.median(a[0, ev] - a[7, ev]), np.median(a[8, ev] - a[0, ev]),
+                                  np.median(a[9, ev] - a[8, ev]), np.median(np.diff(a[7, ev]))))
