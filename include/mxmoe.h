@@ -228,6 +228,30 @@ mxm_status mxm_ep_pack(const void* x, int64_t T, int32_t d, const int32_t* topk_
 mxm_status mxm_ep_combine(const void* back, const int32_t* pos, const int32_t* dest_offsets, int32_t G, int64_t T,
                           int32_t d, const void* y_shared, void* y, mxm_stream stream);
 
+/* ---------------------------------------------------------------- expert parallelism through the C ABI
+ * One MoE layer sharded by experts over an NCCL communicator (Eq. 2 is a sum over experts,
+ * P:71-73). `local`: this rank's routed experts [rank*E/G, (rank+1)*E/G) as a layer with n_shared = 0; `shared`:
+ * the replicated shared experts as a layer of n_shared "routed" experts with n_shared = 0 (or NULL). nccl_comm is
+ * a ncclComm_t borrowed from the caller (e.g. torch's ProcessGroupNCCL._comm_ptr()); it is never destroyed here.
+ * [sync] create / [sync] free: */
+typedef struct mxm_ep mxm_ep;
+mxm_status mxm_ep_init(mxm_layer* local, mxm_layer* shared, void* nccl_comm, int32_t n_global_experts, mxm_ep** out);
+void mxm_ep_free(mxm_ep* ep);
+/* [sync] workspace bytes for T own tokens, top_k routes and at most max_recv_rows rows received from all ranks
+ * (<= world_size * T; each token is sent once per destination rank hosting one of its experts). */
+mxm_status mxm_ep_workspace_bytes(const mxm_ep* ep, int64_t T, int32_t top_k, int64_t max_recv_rows, int64_t* bytes);
+/* Same arguments and result as mxm_moe_group_gemm with GLOBAL expert ids, for this rank's T tokens: the counts are
+ * exchanged with NCCL (one host synchronisation for the all-to-all-v split sizes, v1), rows + local (id, weight)
+ * are dispatched with grouped ncclSend/ncclRecv, the local group-GEMM runs on the received rows, the partial
+ * outputs return, the shared experts run on the own tokens, and y = bf16(sum over destination ranks ascending of
+ * the returned partials + shared), fixed order. MXM_E_CONFIG if more than max_recv_rows rows arrive;
+ * MXM_E_NCCL on a communicator error. Every rank of the communicator must call it (collective). */
+mxm_status mxm_ep_moe_group_gemm(mxm_ep* ep, const void* x, int64_t T, int32_t top_k, const int32_t* topk_ids,
+                                 const float* topk_w, const float* shared_w, void* y, void* workspace, int64_t ws_bytes,
+                                 int64_t max_recv_rows, mxm_stream stream);
+/* [sync] read and clear the EP workspace's error word (bad expert ids in topk_ids -> MXM_E_DATA). */
+mxm_status mxm_ep_poll_device_error(const mxm_ep* ep, const void* workspace, mxm_stream stream, int32_t* code);
+
 /* Thread-local message for the last error returned on this thread. */
 const char* mxm_last_error(void);
 /* Library version string. */

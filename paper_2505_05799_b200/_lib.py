@@ -72,6 +72,11 @@ SIGNATURES = {
     "mxm_profile_scratch_bytes": (C.c_int, [_P, C.POINTER(_I64)]),
     "mxm_profile_tile_costs": (C.c_int, [_P, _P, _I64, _P, _P]),
     "mxm_layer_set_tile_costs": (C.c_int, [_P, _P]),
+    "mxm_ep_init": (C.c_int, [_P, _P, _P, _I32, C.POINTER(_P)]),
+    "mxm_ep_free": (None, [_P]),
+    "mxm_ep_workspace_bytes": (C.c_int, [_P, _I64, _I32, _I64, C.POINTER(_I64)]),
+    "mxm_ep_moe_group_gemm": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _I64, _I64, _P]),
+    "mxm_ep_poll_device_error": (C.c_int, [_P, _P, _P, C.POINTER(_I32)]),
     "mxm_last_error": (C.c_char_p, []),
     "mxm_version": (C.c_char_p, []),
 }

@@ -18,6 +18,17 @@ FLAGS = [
 ]
 
 
+def _nccl_dir() -> str:
+    """NCCL 2.28 of the torch wheel (nvidia-nccl-cu12): headers + libnccl.so.2 (the EP C ABI's collectives)."""
+    import nvidia.nccl
+    return list(nvidia.nccl.__path__)[0]
+
+
+NCCL = _nccl_dir()
+FLAGS += ["-I" + os.path.join(NCCL, "include"), "-L" + os.path.join(NCCL, "lib"), "-l:libnccl.so.2",
+          "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -28,18 +39,34 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel (gemm.cu dominates), then link libmxmoe.so."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="mxmoe_build_")
+    compile_flags = [f for f in FLAGS if f not in ("-shared", "-l:libnccl.so.2", "-Xlinker")
+                     and not f.startswith("-rpath") and not f.startswith("-L")]
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(tmp, src.replace(".cu", ".o"))
+        cmd = [NVCC, *compile_flags, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        procs.append((obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    objs = []
+    for obj, pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError("nvcc failed compiling " + os.path.basename(obj))
+        if verbose:
+            sys.stderr.write(err)
+        objs.append(obj)
+    link = [NVCC, *FLAGS, "-o", LIB + ".tmp", *objs]
+    r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libmxmoe.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libmxmoe.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <nccl.h>
 
 #include <cstdio>
 #include <cstring>
@@ -667,6 +668,208 @@ mxm_status mxm_debug_task_stats(const mxm_layer* l, const void* ws, int64_t T, i
   MXM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   *n_tasks = meta[0];
   *n_executed = meta[6];
+  return MXM_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- expert parallelism through the C ABI (step S9)
+// v1 of SURVEY §8(e): NCCL all-to-all of per-destination counts (one host sync for the split sizes), grouped
+// ncclSend / ncclRecv all-to-all-v of the deduplicated token rows with their local (id, weight) metadata, the local
+// routed group-GEMM, the reverse all-to-all-v of the partial outputs, the shared experts on the own tokens, and
+// the fixed-order combine. The communicator is borrowed (never destroyed here).
+struct mxm_ep {
+  mxm_layer* local = nullptr;
+  mxm_layer* shared = nullptr;
+  ncclComm_t comm = nullptr;
+  int G = 1, rank = 0, E = 0;
+};
+
+namespace {
+struct EpLayout {
+  int64_t err, dest_counts, recv_counts, dest_off, pos, send_x, send_ids, send_w, send_src, recv_x, recv_ids, recv_w,
+      recv_y, back, sid, ones, y_sh, ws_local, ws_shared, total, ws_local_bytes, ws_shared_bytes;
+};
+EpLayout ep_layout(const mxm_ep* ep, int64_t T, int k, int64_t max_recv) {
+  EpLayout w{};
+  const int64_t G = ep->G, d = ep->local->d, S = ep->shared ? ep->shared->E : 0;
+  const int64_t max_send = T * (k < G ? k : G);
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o += align256(bytes > 0 ? bytes : 1);
+    return at;
+  };
+  w.err = take(256);
+  w.dest_counts = take(4 * G);
+  w.recv_counts = take(4 * G);
+  w.dest_off = take(4 * (G + 1));
+  w.pos = take(4 * T * G);
+  w.send_x = take(2 * max_send * d);
+  w.send_ids = take(4 * max_send * k);
+  w.send_w = take(4 * max_send * k);
+  w.send_src = take(4 * max_send);
+  w.recv_x = take(2 * max_recv * d);
+  w.recv_ids = take(4 * max_recv * k);
+  w.recv_w = take(4 * max_recv * k);
+  w.recv_y = take(2 * max_recv * d);
+  w.back = take(2 * max_send * d);
+  w.sid = take(4 * T * (S > 0 ? S : 1));
+  w.ones = take(4 * T * (S > 0 ? S : 1));
+  w.y_sh = take(2 * T * d);
+  w.ws_local_bytes = make_layout(ep->local, max_recv, k).total;
+  w.ws_local = take(w.ws_local_bytes);
+  w.ws_shared_bytes = S > 0 ? make_layout(ep->shared, T, (int)S).total : 0;
+  w.ws_shared = take(w.ws_shared_bytes);
+  w.total = o;
+  return w;
+}
+mxm_status nccl_fail(ncclResult_t r, const char* where) {
+  g_err = std::string(where) + ": " + ncclGetErrorString(r);
+  return MXM_E_NCCL;
+}
+#define MXM_NCCL(call)                                  \
+  do {                                                  \
+    ncclResult_t _r = (call);                           \
+    if (_r != ncclSuccess) return nccl_fail(_r, #call); \
+  } while (0)
+}  // namespace
+
+extern "C" {
+
+mxm_status mxm_ep_init(mxm_layer* local, mxm_layer* shared, void* nccl_comm, int32_t n_global_experts, mxm_ep** out) {
+  if (!local || !nccl_comm || !out) return fail(MXM_E_CONFIG, "null argument");
+  if (local->S != 0) return fail(MXM_E_CONFIG, "the local layer holds routed experts only (shared go in `shared`)");
+  if (shared && (shared->S != 0 || shared->d != local->d)) return fail(MXM_E_CONFIG, "shared layer mismatch");
+  auto* ep = new mxm_ep();
+  ep->comm = reinterpret_cast<ncclComm_t>(nccl_comm);
+  ncclResult_t r = ncclCommCount(ep->comm, &ep->G);
+  if (r == ncclSuccess) r = ncclCommUserRank(ep->comm, &ep->rank);
+  if (r != ncclSuccess) {
+    delete ep;
+    return nccl_fail(r, "ncclCommCount/UserRank");
+  }
+  if (n_global_experts <= 0 || n_global_experts % ep->G != 0 || local->E != n_global_experts / ep->G) {
+    delete ep;
+    return fail(MXM_E_CONFIG, "local layer must hold n_global_experts / world_size routed experts");
+  }
+  ep->local = local;
+  ep->shared = shared;
+  ep->E = n_global_experts;
+  *out = ep;
+  return MXM_OK;
+}
+
+void mxm_ep_free(mxm_ep* ep) { delete ep; }
+
+mxm_status mxm_ep_poll_device_error(const mxm_ep* ep, const void* ws, mxm_stream stream, int32_t* code) {
+  if (!ep || !ws || !code) return fail(MXM_E_CONFIG, "null argument");
+  int32_t v = 0;  // the EP workspace starts with its error word (bad expert ids seen by the dispatch)
+  MXM_CUDA(cudaMemcpyAsync(&v, ws, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  MXM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  MXM_CUDA(cudaMemsetAsync(const_cast<void*>(ws), 0, 4, (cudaStream_t)stream));
+  *code = v ? MXM_E_DATA : MXM_OK;
+  return MXM_OK;
+}
+
+mxm_status mxm_ep_workspace_bytes(const mxm_ep* ep, int64_t T, int32_t k, int64_t max_recv_rows, int64_t* bytes) {
+  if (!ep || !bytes || T < 0 || k <= 0 || k > 32 || max_recv_rows < 0) return fail(MXM_E_CONFIG, "bad argument");
+  *bytes = ep_layout(ep, T, k, max_recv_rows).total;
+  return MXM_OK;
+}
+
+mxm_status mxm_ep_moe_group_gemm(mxm_ep* ep, const void* x, int64_t T, int32_t k, const int32_t* topk_ids,
+                                 const float* topk_w, const float* shared_w, void* y, void* ws, int64_t ws_bytes,
+                                 int64_t max_recv_rows, mxm_stream stream) {
+  if (!ep || !ws || (T > 0 && (!x || !topk_ids || !topk_w || !y))) return fail(MXM_E_CONFIG, "null argument");
+  if (k <= 0 || k > 32 || T < 0) return fail(MXM_E_CONFIG, "bad top_k / T");
+  const EpLayout w = ep_layout(ep, T, k, max_recv_rows);
+  if (ws_bytes < w.total) return fail(MXM_E_CONFIG, "EP workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* b = reinterpret_cast<uint8_t*>(ws);
+  auto P = [&](int64_t off) -> void* { return (void*)(b + off); };
+  const int G = ep->G, d = ep->local->d, S = ep->shared ? ep->shared->E : 0;
+  int32_t* dest_counts = (int32_t*)P(w.dest_counts);
+  int32_t* recv_counts = (int32_t*)P(w.recv_counts);
+  int32_t* pos = (int32_t*)P(w.pos);
+  // 1. per-destination deduplicated counts and slots, exchanged
+  MXM_CUDA(launch_ep_route(topk_ids, T, k, ep->E, G, dest_counts, pos, (int32_t*)P(w.err), st));
+  MXM_NCCL(ncclGroupStart());
+  for (int r = 0; r < G; ++r) {
+    MXM_NCCL(ncclSend(dest_counts + r, 1, ncclInt32, r, ep->comm, st));
+    MXM_NCCL(ncclRecv(recv_counts + r, 1, ncclInt32, r, ep->comm, st));
+  }
+  MXM_NCCL(ncclGroupEnd());
+  std::vector<int32_t> sc(G), rc(G);
+  MXM_CUDA(cudaMemcpyAsync(sc.data(), dest_counts, 4 * G, cudaMemcpyDeviceToHost, st));
+  MXM_CUDA(cudaMemcpyAsync(rc.data(), recv_counts, 4 * G, cudaMemcpyDeviceToHost, st));
+  MXM_CUDA(cudaStreamSynchronize(st));  // v1: the split sizes of the all-to-all-v live on the host
+  std::vector<int64_t> so(G + 1, 0), ro(G + 1, 0);
+  for (int r = 0; r < G; ++r) {
+    so[r + 1] = so[r] + sc[r];
+    ro[r + 1] = ro[r] + rc[r];
+  }
+  const int64_t S_send = so[G], R = ro[G];
+  if (R > max_recv_rows) return fail(MXM_E_CONFIG, "received rows exceed max_recv_rows");
+  std::vector<int32_t> so32(G + 1);
+  for (int r = 0; r <= G; ++r) so32[r] = (int32_t)so[r];
+  int32_t* dest_off = (int32_t*)P(w.dest_off);
+  MXM_CUDA(cudaMemcpyAsync(dest_off, so32.data(), 4 * (G + 1), cudaMemcpyHostToDevice, st));
+  // 2. send buffers (rows by (destination, token)) and the all-to-all-v of rows / local ids / weights
+  MXM_CUDA(launch_ep_pack(x, T, d, topk_ids, topk_w, k, ep->E, G, pos, dest_off, P(w.send_x), (int32_t*)P(w.send_ids),
+                          (float*)P(w.send_w), (int32_t*)P(w.send_src), st));
+  MXM_NCCL(ncclGroupStart());
+  for (int r = 0; r < G; ++r) {
+    if (sc[r]) {
+      MXM_NCCL(ncclSend((uint16_t*)P(w.send_x) + so[r] * d, (size_t)sc[r] * d, ncclBfloat16, r, ep->comm, st));
+      MXM_NCCL(ncclSend((int32_t*)P(w.send_ids) + so[r] * k, (size_t)sc[r] * k, ncclInt32, r, ep->comm, st));
+      MXM_NCCL(ncclSend((float*)P(w.send_w) + so[r] * k, (size_t)sc[r] * k, ncclFloat32, r, ep->comm, st));
+    }
+    if (rc[r]) {
+      MXM_NCCL(ncclRecv((uint16_t*)P(w.recv_x) + ro[r] * d, (size_t)rc[r] * d, ncclBfloat16, r, ep->comm, st));
+      MXM_NCCL(ncclRecv((int32_t*)P(w.recv_ids) + ro[r] * k, (size_t)rc[r] * k, ncclInt32, r, ep->comm, st));
+      MXM_NCCL(ncclRecv((float*)P(w.recv_w) + ro[r] * k, (size_t)rc[r] * k, ncclFloat32, r, ep->comm, st));
+    }
+  }
+  MXM_NCCL(ncclGroupEnd());
+  // 3. the local routed experts on the received rows
+  if (R > 0) {
+    mxm_status s = run_group_gemm(ep->local, P(w.recv_x), R, k, (const int32_t*)P(w.recv_ids),
+                                  (const float*)P(w.recv_w), nullptr, P(w.recv_y), P(w.ws_local), w.ws_local_bytes,
+                                  stream, nullptr);
+    if (s != MXM_OK) return s;
+  }
+  // 4. partial outputs back to their source ranks, in send order
+  MXM_NCCL(ncclGroupStart());
+  for (int r = 0; r < G; ++r) {
+    if (rc[r]) MXM_NCCL(ncclSend((uint16_t*)P(w.recv_y) + ro[r] * d, (size_t)rc[r] * d, ncclBfloat16, r, ep->comm, st));
+    if (sc[r]) MXM_NCCL(ncclRecv((uint16_t*)P(w.back) + so[r] * d, (size_t)sc[r] * d, ncclBfloat16, r, ep->comm, st));
+  }
+  MXM_NCCL(ncclGroupEnd());
+  // 5. shared experts on the own tokens (top-k = S, every token routed to all of them with weight shared_w)
+  void* y_sh = nullptr;
+  if (S > 0 && T > 0) {
+    std::vector<int32_t> sid((size_t)T * S);
+    for (int64_t t = 0; t < T; ++t)
+      for (int s2 = 0; s2 < S; ++s2) sid[(size_t)t * S + s2] = s2;
+    MXM_CUDA(cudaMemcpyAsync(P(w.sid), sid.data(), 4 * T * S, cudaMemcpyHostToDevice, st));
+    const float* swp = shared_w;
+    if (!swp) {
+      std::vector<float> ones((size_t)T * S, 1.f);
+      MXM_CUDA(cudaMemcpyAsync(P(w.ones), ones.data(), 4 * T * S, cudaMemcpyHostToDevice, st));
+      MXM_CUDA(cudaStreamSynchronize(st));  // host staging buffers go out of scope
+      swp = (const float*)P(w.ones);
+    } else {
+      MXM_CUDA(cudaStreamSynchronize(st));
+    }
+    y_sh = P(w.y_sh);
+    mxm_status s = run_group_gemm(ep->shared, x, T, S, (const int32_t*)P(w.sid), swp, nullptr, y_sh, P(w.ws_shared),
+                                  w.ws_shared_bytes, stream, nullptr);
+    if (s != MXM_OK) return s;
+  }
+  // 6. fixed-order combine over destinations + shared
+  if (T > 0) MXM_CUDA(launch_ep_combine(P(w.back), pos, dest_off, G, T, d, y_sh, y, st));
+  (void)S_send;
   return MXM_OK;
 }
 

@@ -31,12 +31,24 @@ from . import MoELayer, Scheme, _ptr, _stream, check, load
 class CudaEpOps:
     """The libmxmoe EP kernels (device tensors)."""
 
+    def __init__(self):
+        self.err = None  # device error word of the dispatch (bad expert ids -> MXM_E_DATA), see poll_error
+
     def route(self, ids: torch.Tensor, E: int, G: int):
         T, k = ids.shape
         counts = torch.zeros(G, dtype=torch.int32, device=ids.device)
         pos = torch.empty(T, G, dtype=torch.int32, device=ids.device)
-        check(load().mxm_ep_route(_ptr(ids), T, k, E, G, _ptr(counts), _ptr(pos), None, _stream()))
+        if self.err is None:
+            self.err = torch.zeros(1, dtype=torch.int32, device=ids.device)
+        check(load().mxm_ep_route(_ptr(ids), T, k, E, G, _ptr(counts), _ptr(pos), _ptr(self.err), _stream()))
         return counts, pos
+
+    def poll_error(self) -> int:
+        if self.err is None:
+            return 0
+        v = int(self.err.item())
+        self.err.zero_()
+        return v
 
     def pack(self, x, ids, w, pos, dest_off, E, G, S_total):
         T, k = ids.shape
@@ -119,3 +131,58 @@ class ExpertParallelMoE:
             swt = shared_w if shared_w is not None else torch.ones(T, self.S, dtype=torch.float32, device=dev)
             ysh = self.shared(x, sid, swt.contiguous())
         return self.ops.combine(back, pos, dest_off, G, ysh, T, d)
+
+
+class CAbiExpertParallelMoE:
+    """The same expert-parallel block through the library's own C ABI (mxm_ep_init / mxm_ep_moe_group_gemm):
+    counts, rows and partial outputs move with NCCL inside libmxmoe on torch's communicator (_comm_ptr()),
+    so a call is one library entry point per rank."""
+
+    def __init__(self, local: MoELayer, shared: Optional[MoELayer], n_routed: int, group=None):
+        from torch.distributed.distributed_c10d import _get_default_group
+        pg = group if group is not None else _get_default_group()
+        comm = pg._get_backend(torch.device("cuda"))._comm_ptr()
+        self.local, self.shared, self.E = local, shared, n_routed
+        self.G = dist.get_world_size(group)
+        h = C.c_void_p()
+        check(load().mxm_ep_init(local._h, shared._h if shared is not None else None, C.c_void_p(comm), n_routed,
+                                 C.byref(h)))
+        self._h = h
+        self._ws = None
+
+    @classmethod
+    def from_weights(cls, n_routed: int, n_shared: int, hidden: int, inter: int, shared_inter: int,
+                     weights, table, group=None) -> "CAbiExpertParallelMoE":
+        py = ExpertParallelMoE.from_weights(n_routed, n_shared, hidden, inter, shared_inter, weights, table, group)
+        return cls(py.local, py.shared, n_routed, group)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                load().mxm_ep_free(self._h)
+        except Exception:
+            pass
+
+    def workspace(self, T: int, k: int, max_recv: int) -> torch.Tensor:
+        nb = C.c_int64()
+        check(load().mxm_ep_workspace_bytes(self._h, T, k, max_recv, C.byref(nb)))
+        if self._ws is None or self._ws.numel() < nb.value:
+            self._ws = torch.zeros(nb.value, dtype=torch.uint8, device="cuda")
+        return self._ws
+
+    def __call__(self, x: torch.Tensor, topk_ids: torch.Tensor, topk_w: torch.Tensor,
+                 shared_w: Optional[torch.Tensor] = None, max_recv: Optional[int] = None) -> torch.Tensor:
+        T, k = topk_ids.shape
+        assert x.dtype == torch.bfloat16 and x.is_contiguous() and topk_ids.dtype == torch.int32
+        assert topk_ids.is_contiguous() and topk_w.dtype == torch.float32 and topk_w.is_contiguous()
+        max_recv = self.G * T if max_recv is None else max_recv
+        ws = self.workspace(T, k, max_recv)
+        y = torch.empty(T, self.local.hidden, dtype=torch.bfloat16, device=x.device)
+        check(load().mxm_ep_moe_group_gemm(self._h, _ptr(x), T, k, _ptr(topk_ids), _ptr(topk_w), _ptr(shared_w),
+                                           _ptr(y), _ptr(ws), ws.numel(), max_recv, _stream()))
+        return y
+
+    def poll_error(self) -> int:
+        code = C.c_int32()
+        check(load().mxm_ep_poll_device_error(self._h, _ptr(self._ws), _stream(), C.byref(code)))
+        return code.value

@@ -101,3 +101,42 @@ def test_ep_loopback_equals_unsharded(mx, G):
     rows = np.arange(0, T, 4)
     ref = oracle_run(oracle_layer(case), case, rows=rows)
     assert row_rel_err(y[rows], ref) <= 1e-2
+
+
+def test_ep_c_abi_nccl_world1(mx):
+    """mxm_ep_init / mxm_ep_moe_group_gemm on a real NCCL communicator (torch ProcessGroupNCCL, world size 1 on the
+    one reachable GPU): the library's own NCCL dispatch / combine path equals the torch-orchestrated EP path bitwise
+    (same kernels, same order), matches the oracle, and reports bad expert ids through its error word."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2505_05799_b200.ep import CAbiExpertParallelMoE, ExpertParallelMoE
+    if not dist.is_initialized():
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    cfg = C.LayerConfig("ep1", 8, 1, 256, 512, 384, 2, 96)
+    table = ([[C.WA(4, 128)] * 3] * 3 + [[C.WO(4, 128)] * 3] * 3 + [[C.WA(8, -1)] * 3] * 2 + [[C.WO(2, -1)] * 3])
+    case = make_case(cfg, table, 96, seed=12)
+    W = [[bf16_tensor(b) for b in blk] for blk in case["weights"]]
+    py = ExpertParallelMoE.from_weights(cfg.n_routed, cfg.n_shared, cfg.hidden, cfg.inter, cfg.shared_inter, W, table)
+    cab = CAbiExpertParallelMoE(py.local, py.shared, cfg.n_routed)
+    x = bf16_tensor(case["x"])
+    ids = torch.from_numpy(case["ids"]).cuda()
+    w = torch.from_numpy(case["w"]).cuda()
+    sw = torch.from_numpy(case["shared_w"]).cuda()
+    y_py = py(x, ids, w, sw)
+    y_c = cab(x, ids, w, sw)
+    torch.cuda.synchronize()
+    assert torch.equal(y_py, y_c)
+    ref = oracle_run(oracle_layer(case), case)
+    assert row_rel_err(y_c.float().cpu().numpy().astype(np.float64), ref) <= 1e-2
+    assert cab.poll_error() == 0
+    bad = ids.clone()
+    bad[3, 0] = 99
+    cab(x, bad, w, sw)
+    assert cab.poll_error() == 4
+    del cab, py
+    dist.destroy_process_group()
