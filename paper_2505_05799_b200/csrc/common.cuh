@@ -94,7 +94,10 @@ static_assert(sizeof(Task) == 16, "task size");
 // slices write fp32 partials, the last-arriving slice reduces them in fixed slice order (deterministic).
 // A phase-2 task's ntile holds the tile (pair) index in bits 0-9 and the slice in bits 10-13.
 constexpr int kSplitMax = 4;
-constexpr int kSplitRows = 512;  // split only when the launch has <= this many route rows (partial buffer size)
+#ifndef MXM_SPLIT_ROWS
+#define MXM_SPLIT_ROWS 512
+#endif
+constexpr int kSplitRows = MXM_SPLIT_ROWS;  // split only when the launch has <= this many route rows (0: never)
 __host__ __device__ inline int task_tile(const Task& t) { return t.phase == 2 ? (t.ntile & 0x3FF) : t.ntile; }
 __host__ __device__ inline int task_slice(const Task& t) { return t.phase == 2 ? (t.ntile >> 10) : 0; }
 __host__ __device__ inline bool down_splittable(const ExpertDesc& e) {

@@ -1043,8 +1043,7 @@ __device__ __forceinline__ void stage_scales(const GemmParams& p, const Task& t,
         reinterpret_cast<float*>(slotp + kSlotB)[c] = s.f8 ? __fmul_rn(-8.f * (float)qs[h], sa[h]) : 0.f;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ctl.sready[ss]);
+    mbar_arrive(&ctl.sready[ss]);  // every lane releases its own slot writes
     ++xsidx;
   }
 }
@@ -1078,8 +1077,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     }
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(&ctl.sfull[i], 1);
-      mbar_init(&ctl.sempty[i], 8);  // the 8 epilogue warps
-      mbar_init(&ctl.sready[i], 1);  // the scale-staging warp 3 (drain factors staged)
+      mbar_init(&ctl.sempty[i], 256);  // every thread of the 8 epilogue warps
+      mbar_init(&ctl.sready[i], 32);  // every lane of the scale-staging warp 3 (drain factors staged)
     }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&ctl.accf[i], 1);
@@ -1726,10 +1725,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 #endif
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-              mbar_arrive(&ctl.acce[b0]);
-              if (s.g128) mbar_arrive(&ctl.sempty[ss]);
-            }
+            if (lane == 0) mbar_arrive(&ctl.acce[b0]);
+            if (s.g128) mbar_arrive(&ctl.sempty[ss]);  // every lane: its slot reads are done
             if (threadIdx.x == 256) TR(6, n_tr_e);
             ++n_tr_e;
             if (s.g128) ++sidx;
