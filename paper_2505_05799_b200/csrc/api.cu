@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -78,6 +79,11 @@ int num_sms() {
 }
 
 int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
+// A/B switch from the environment (e.g. MXM_GATHER_ROWS=1: the row-major S2 gather)
+bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
+}
 }  // namespace
 
 struct mxm_layer {
@@ -86,6 +92,7 @@ struct mxm_layer {
   std::vector<ExpertDesc> ex;
   ExpertDesc* ex_dev;
   bool need_xb, need_xqa, need_xqb, need_hq;
+  ActFormats fm;  // distinct gate/up input formats (token-major gather); fm.n = 0: row-major gather
   // optional per-stage timing: kProfEv events per slot recorded around the launches of a call
   int prof_n = 0;
   void* prof_counters = nullptr;  // device [grid][16] u64 wait-site cycle counters (debug)
@@ -325,6 +332,33 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
     }
     if (e.blk[2].in_slot == 1) l->need_hq = true;
   }
+  // distinct gate/up input formats: the token-major gather quantizes each token once per format
+  {
+    ActFormats fm{};
+    bool ok = l->d % 128 == 0 && l->d <= 4096 && S <= 8;
+    for (int v = 0; v < V && ok; ++v) {
+      for (int j = 0; j < 2 && ok; ++j) {
+        const LinDesc& L = l->ex[v].blk[j];
+        const int b = L.in_slot == 0 ? 16 : L.a_bits, g = L.in_slot == 0 ? 0 : L.a_group;
+        const int e4 = L.in_slot == 0 ? 0 : (kind_is_f8(L.geo.kind) ? 1 : 0);
+        if (L.in_slot != 0 && g != 128 && g != -1) ok = false;
+        int i = 0;
+        while (i < fm.n && !(fm.a_bits[i] == b && fm.a_group[i] == g && fm.e4[i] == e4)) ++i;
+        if (i == fm.n) {
+          if (fm.n == 6) {
+            ok = false;
+          } else {
+            fm.a_bits[i] = b;
+            fm.a_group[i] = g;
+            fm.e4[i] = e4;
+            ++fm.n;
+          }
+        }
+      }
+    }
+    if (!ok) fm.n = 0;
+    l->fm = fm;
+  }
   if (tile_costs) {  // measured per-(expert, token tile) m-tile group costs (mxm_profile_tile_costs), ms
     const float* c = reinterpret_cast<const float*>(tile_costs);
     for (int v = 0; v < V; ++v)
@@ -416,9 +450,15 @@ static mxm_status run_group_gemm(const mxm_layer* l, const void* x, int64_t T, i
                        (int32_t*)P(w.hq_done), no_split ? nullptr : (int32_t*)P(w.red_cnt), ml->side));
   MXM_CUDA(cudaEventRecord(ml->ev_join, ml->side));
   // S2 activation quantize + gather
-  MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
+  if (l->fm.n > 0 && k + l->S <= 32 && !getenv_flag("MXM_GATHER_ROWS")) {
+    MXM_CUDA(launch_gather_tok(x, l->d, T, k, l->S, l->E, inv, row_exp, l->ex_dev, l->fm, w.R, P(w.Xb), P(w.XqA),
                                (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), (int32_t*)P(w.XcA), (int32_t*)P(w.XcB),
                                (uint32_t*)P(w.hmax), st));
+  } else {
+    MXM_CUDA(launch_gather_quant(x, l->d, row_src, row_exp, v_off, l->V, l->ex_dev, w.R, P(w.Xb), P(w.XqA),
+                                 (float*)P(w.XsA), P(w.XqB), (float*)P(w.XsB), (int32_t*)P(w.XcA),
+                                 (int32_t*)P(w.XcB), (uint32_t*)P(w.hmax), st));
+  }
   mark(2);
   MXM_CUDA(cudaStreamWaitEvent(st, ml->ev_join, 0));
   mark(3);  // the plan's time beyond the gather's (usually ~0)

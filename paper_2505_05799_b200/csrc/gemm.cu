@@ -1043,7 +1043,8 @@ __device__ __forceinline__ void stage_scales(const GemmParams& p, const Task& t,
         reinterpret_cast<float*>(slotp + kSlotB)[c] = s.f8 ? __fmul_rn(-8.f * (float)qs[h], sa[h]) : 0.f;
       }
     }
-    mbar_arrive(&ctl.sready[ss]);  // every lane releases its own slot writes
+    __syncwarp();  // orders every lane's slot writes before lane 0's release
+    if (lane == 0) mbar_arrive(&ctl.sready[ss]);
     ++xsidx;
   }
 }
@@ -1077,8 +1078,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     }
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(&ctl.sfull[i], 1);
-      mbar_init(&ctl.sempty[i], 256);  // every thread of the 8 epilogue warps
-      mbar_init(&ctl.sready[i], 32);  // every lane of the scale-staging warp 3 (drain factors staged)
+      mbar_init(&ctl.sempty[i], 8);  // lane 0 of every epilogue warp (after __syncwarp)
+      mbar_init(&ctl.sready[i], 1);  // lane 0 of the scale-staging warp 3 (drain factors staged)
     }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&ctl.accf[i], 1);
@@ -1726,7 +1727,9 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&ctl.acce[b0]);
-            if (s.g128) mbar_arrive(&ctl.sempty[ss]);  // every lane: its slot reads are done
+            // the warp's slot reads are ordered before lane 0's release by the __syncwarp above (one arrival per
+            // warp: per-lane arrivals serialise on the barrier word)
+            if (s.g128 && lane == 0) mbar_arrive(&ctl.sempty[ss]);
             if (threadIdx.x == 256) TR(6, n_tr_e);
             ++n_tr_e;
             if (s.g128) ++sidx;

@@ -49,6 +49,16 @@ cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T
                               const float* shared_w, int32_t* counts, int32_t* offsets, int32_t* v_off, int32_t* perm,
                               int32_t* row_src, float* row_w, int32_t* row_exp, int32_t* inv, int32_t* err,
                               void* scratch, cudaStream_t st);
+// distinct gate/up input formats of a layer (token-major gather): a_bits 16 = bf16 copy, else the dynamic
+// quantizer's (a_bits, a_group (-1 per token / 128), e4m3 codes)
+struct ActFormats {
+  int n;
+  int a_bits[6], a_group[6], e4[6];
+};
+cudaError_t launch_gather_tok(const void* x, int d, int64_t T, int k, int S, int E, const int32_t* inv,
+                              const int32_t* row_exp, const ExpertDesc* ex, const ActFormats& fm, int64_t R, void* Xb,
+                              void* XqA, float* XsA, void* XqB, float* XsB, int32_t* XcA, int32_t* XcB, uint32_t* hmax,
+                              cudaStream_t st);
 cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, const int32_t* row_exp,
                                 const int32_t* v_off, int V, const ExpertDesc* ex, int64_t R, void* Xb, void* XqA,
                                 float* XsA, void* XqB, float* XsB, int32_t* XcA, int32_t* XcB, uint32_t* hmax,

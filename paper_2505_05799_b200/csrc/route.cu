@@ -212,6 +212,144 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
   }
 }
 
+// ---- S2, token-major: one warp per (token, input format). The dynamic quantizer's result depends only on the
+// token's row and the format (a_bits, group, code encoding), not on the expert, so each token is quantized once
+// per format in use ("dynamically quantized at runtime according to the corresponding allocated scheme")
+// and the codes / scales / code sums are stored to every route row of the token whose gate or up block reads
+// that format (k routed rows via inv[], S shared rows s*T + t). Same arithmetic as quant_row_warp (DESIGN R9):
+// every stored row is bit-identical to the row-major kernel's. Format a_bits 16 = the bf16 row copy (Xb).
+template <int MAXG>
+__global__ void __launch_bounds__(256) gather_tok_kernel(
+    const uint16_t* __restrict__ x, int d, int64_t T, int k, int S, int E, const int32_t* __restrict__ inv,
+    const int32_t* __restrict__ row_exp, const ExpertDesc* __restrict__ ex, ActFormats fm, int64_t R,
+    uint16_t* __restrict__ Xb, int8_t* __restrict__ XqA, float* __restrict__ XsA, int8_t* __restrict__ XqB,
+    float* __restrict__ XsB, int32_t* __restrict__ XcA, int32_t* __restrict__ XcB, uint32_t* __restrict__ hmax) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (w >= T * fm.n) return;
+  const int64_t t = w / fm.n;
+  const int f = (int)(w % fm.n);
+  const int fb = fm.a_bits[f], fg = fm.a_group[f];
+  const bool fe = fm.e4[f] != 0;
+  // lane j < k + S resolves route j of the token: its row and the slots (1 / 2) of gate / up that read format f
+  int64_t row = -1;
+  int sl0 = -1, sl1 = -1;  // slot written for the gate / up input (-1: another format)
+  if (lane < k + S) {
+    row = lane < k ? (int64_t)inv[t * k + lane] : (int64_t)(lane - k) * T + t;
+    if (row >= 0) {
+      const int v = lane < k ? row_exp[row] : E + (lane - k);
+      const LinDesc& L0 = ex[v].blk[0];
+      const LinDesc& L1 = ex[v].blk[1];
+      auto match = [&](const LinDesc& L) {
+        if (L.in_slot == 0) return fb == 16;
+        return fb == L.a_bits && fg == L.a_group && fe == kind_is_f8(L.geo.kind);
+      };
+      if (match(L0)) sl0 = L0.in_slot;
+      if (L1.in_slot != L0.in_slot && match(L1)) sl1 = L1.in_slot;
+    }
+  }
+  const unsigned todo = __ballot_sync(0xffffffffu, sl0 >= 0 || sl1 >= 0);
+  if (todo == 0) return;
+  const int nch = d / 128;
+  const uint16_t* src = x + t * d;
+  uint2 v[MAXG];
+#pragma unroll
+  for (int i = 0; i < MAXG; ++i)
+    if (i < nch) v[i] = *reinterpret_cast<const uint2*>(src + 128 * i + 4 * lane);
+  if (fb == 16) {  // bf16 copy into every weight-only / 16-bit route row of the token
+    for (unsigned m = todo; m; m &= m - 1) {
+      const int j = __ffs(m) - 1;
+      const int64_t r = __shfl_sync(0xffffffffu, row, j);
+      const int g0 = __shfl_sync(0xffffffffu, sl0, j);
+      uint16_t* dst = Xb + r * d;
+#pragma unroll
+      for (int i = 0; i < MAXG; ++i)
+        if (i < nch) *reinterpret_cast<uint2*>(dst + 128 * i + 4 * lane) = v[i];
+      if (lane == 0 && g0 >= 0 && hmax) hmax[r] = 0u;
+    }
+    return;
+  }
+  const float fq = (float)((1 << (fb - 1)) - 1);
+  auto absmax4 = [](uint2 a) {
+    return fmaxf(fmaxf(fabsf(bf16_bits_to_float(a.x & 0xFFFFu)), fabsf(bf16_bits_to_float(a.x >> 16))),
+                 fmaxf(fabsf(bf16_bits_to_float(a.y & 0xFFFFu)), fabsf(bf16_bits_to_float(a.y >> 16))));
+  };
+  auto quant4 = [&](uint2 a, float r, int& qsum) {
+    const float fv[4] = {bf16_bits_to_float(a.x & 0xFFFFu), bf16_bits_to_float(a.x >> 16),
+                         bf16_bits_to_float(a.y & 0xFFFFu), bf16_bits_to_float(a.y >> 16)};
+    uint32_t packed = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float q = rintf(__fmul_rn(fv[j], r));
+      q = fminf(fmaxf(q, -fq), fq);
+      qsum += (int)q;
+      packed |= (fe ? code_byte<true>((int)q) : code_byte<false>((int)q)) << (8 * j);
+    }
+    return packed;
+  };
+  uint32_t code[MAXG];
+  float my_s = 1.f;  // g128: lane i holds group i's scale and code sum; per token: lane 0 the row's
+  int my_qs = 0;
+  if (fg == 128) {
+#pragma unroll
+    for (int i = 0; i < MAXG; ++i) {
+      if (i < nch) {
+        const float amax = warp_max(absmax4(v[i]));
+        float r = 0.f, s = 1.f;
+        if (amax > 0.f) {
+          r = __fdiv_rn(fq, amax);
+          s = __fdiv_rn(amax, fq);
+        }
+        int qsum = 0;
+        code[i] = quant4(v[i], r, qsum);
+        qsum = warp_sum(qsum);
+        if (lane == i) {
+          my_s = s;
+          my_qs = qsum;
+        }
+      }
+    }
+  } else {
+    float amax = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXG; ++i)
+      if (i < nch) amax = fmaxf(amax, absmax4(v[i]));
+    amax = warp_max(amax);
+    float r = 0.f, s = 1.f;
+    if (amax > 0.f) {
+      r = __fdiv_rn(fq, amax);
+      s = __fdiv_rn(amax, fq);
+    }
+    int qsum = 0;
+#pragma unroll
+    for (int i = 0; i < MAXG; ++i)
+      if (i < nch) code[i] = quant4(v[i], r, qsum);
+    my_s = s;
+    my_qs = warp_sum(qsum);
+  }
+  const int ng = fg == 128 ? nch : 1;
+  for (unsigned m = todo; m; m &= m - 1) {
+    const int j = __ffs(m) - 1;
+    const int64_t r = __shfl_sync(0xffffffffu, row, j);
+    const int g0 = __shfl_sync(0xffffffffu, sl0, j), g1 = __shfl_sync(0xffffffffu, sl1, j);
+    for (int b = 0; b < 2; ++b) {
+      const int slot = b == 0 ? g0 : g1;
+      if (slot < 1) continue;
+      int8_t* q = (slot == 1 ? XqA : XqB) + r * d;
+      float* sc = (slot == 1 ? XsA : XsB) + r;  // group-major [g][R]
+      int32_t* qs = (slot == 1 ? XcA : XcB) + r;
+#pragma unroll
+      for (int i = 0; i < MAXG; ++i)
+        if (i < nch) *reinterpret_cast<uint32_t*>(q + 128 * i + 4 * lane) = code[i];
+      if (lane < ng) {
+        sc[(int64_t)lane * R] = my_s;
+        qs[(int64_t)lane * R] = my_qs;
+      }
+    }
+    if (lane == 0 && g0 >= 0 && hmax) hmax[r] = 0u;
+  }
+}
+
 // ---- S8: combine, one block per token; all k + S source rows are resolved first so their loads overlap
 __global__ void combine_kernel(const uint16_t* __restrict__ O, int d, int64_t T, int k, int S,
                                const int32_t* __restrict__ inv, uint16_t* __restrict__ y) {
@@ -295,6 +433,18 @@ cudaError_t launch_gather_quant(const void* x, int d, const int32_t* row_src, co
     gather_quant_kernel<false><<<(unsigned)((R * 32 + 255) / 256), 256, 0, st>>>(
         (const uint16_t*)x, d, row_src, row_exp, v_off, V, ex, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB, XsB,
         XcA, XcB, hmax);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_tok(const void* x, int d, int64_t T, int k, int S, int E, const int32_t* inv,
+                              const int32_t* row_exp, const ExpertDesc* ex, const ActFormats& fm, int64_t R, void* Xb,
+                              void* XqA, float* XsA, void* XqB, float* XsB, int32_t* XcA, int32_t* XcB, uint32_t* hmax,
+                              cudaStream_t st) {
+  if (T <= 0 || fm.n <= 0) return cudaSuccess;
+  const int64_t warps = T * fm.n;
+  gather_tok_kernel<32><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(
+      (const uint16_t*)x, d, T, k, S, E, inv, row_exp, ex, fm, R, (uint16_t*)Xb, (int8_t*)XqA, XsA, (int8_t*)XqB,
+      XsB, XcA, XcB, hmax);
   return cudaGetLastError();
 }
 

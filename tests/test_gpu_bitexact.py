@@ -178,3 +178,26 @@ def test_long_k_bitexact(mx, sch):
     cfg = C.LayerConfig("bxk", 2, 0, 256, 14336, 0, 1, 24)
     case = make_case(cfg, C.uniform_table(cfg, sch), 24, seed=5)
     check_case(mx, case)
+
+
+def test_token_major_gather_equals_row_major(mx, monkeypatch):
+    """S2: the token-major gather (each token quantized once per input format, stored to all its route rows)
+    writes the same bytes as the row-major one (one warp per route row), here with a bf16 slot, three quantized
+    formats (e4m3 per-token and g128, int8 per-token), two input slots and a shared expert."""
+    cfg = C.LayerConfig("bx3", 4, 1, 256, 384, 512, 3, 70)
+    a4g, a4c, a8c = C.WA(4, 128), C.WA(4, -1), C.WA(8, -1)
+    table = [[a4g, a8c, a4g], [a8c, a4g, a4c], [C.WO(4, 128), a4c, a4g], [C.WO(2, 128), C.W16, a8c],
+             [a4c, a4c, a8c]]
+    case = make_case(cfg, table, 70, seed=11)
+    check_case(mx, case)
+    _, lay, ws_tok, _, _ = _run(mx, case)
+    monkeypatch.setenv("MXM_GATHER_ROWS", "1")
+    _, _, ws_row, _, _ = _run(mx, case)
+    R, d = lay["R"], cfg.hidden
+    for key, n in (("xb", 2 * R * d), ("xqa", R * d), ("xqb", R * d), ("xsa", 4 * R * (d // 128)),
+                   ("xsb", 4 * R * (d // 128)), ("xca", 4 * R * (d // 128)), ("xcb", 4 * R * (d // 128))):
+        off = lay[key]
+        if off < 0:
+            continue
+        # only rows that hold a route are defined (rows past the last valid route are never written)
+        assert np.array_equal(ws_tok[off: off + n], ws_row[off: off + n]), key
