@@ -64,7 +64,7 @@ def table_for(cfg, name, T):
     if name == "w16":
         return C.uniform_table(cfg, C.W16)
     for s in ([C.WO(b, g, sy) for b in (2, 3, 4, 8) for g in (64, 128, -1) for sy in (False, True)]
-              + [C.WA(b, g) for b in (4, 5, 8) for g in (128, -1)]):
+              + [C.WA(b, g) for b in (4, 5, 8) for g in (128, -1)] + [C.FP8(g) for g in (128, -1)]):
         if s.name() == name:
             return C.uniform_table(cfg, s)
     raise SystemExit(f"unknown table {name}")

@@ -40,7 +40,11 @@ typedef enum { MXM_OK = 0, MXM_E_CONFIG = 3, MXM_E_DATA = 4, MXM_E_CUDA = 5, MXM
  *   symmetric 1 = scale only; 0 = scale + zero-point (weight-only only)                        */
 typedef struct {
   int32_t w_bits, a_bits, w_group, a_group, symmetric;
+  int32_t fmt; /* MXM_FMT_INT (0): integer codes (the paper's uniform quantizer); MXM_FMT_E4M3 (1): FP8
+                * e4m3 codes for weights and activations (NEXT-4 "FP8 as an extra hardware-supported scheme",
+                * readings R25/R26), w_bits = a_bits = 8, symmetric, w_group = a_group in {-1, 128} */
 } mxm_scheme;
+enum { MXM_FMT_INT = 0, MXM_FMT_E4M3 = 1 };
 
 typedef void* mxm_stream; /* a cudaStream_t */
 
@@ -72,6 +76,33 @@ mxm_status mxm_pack(const mxm_scheme* s, const void* codes, const void* scale, c
 /* Test/debug: dequantize a packed block to float32 w_out[N, K] = q·s + z exactly (q·s sym). */
 mxm_status mxm_dequantize(const mxm_scheme* s, const void* packed, int64_t N, int64_t K, float* w_out,
                           mxm_stream stream);
+
+/* ---- NEXT-4: offline weight preparation (§4.2.3 "randomized Hadamard transformations ... using the
+ * incoherence processing used in QuaRot, then ... GPTQ-based quantization"; "We disabled online rotations").
+ * Readings DESIGN.md R22-R24. Not on the hot path: they produce the codes / scales / zeros mxm_pack consumes.
+ * All arithmetic fp64; every pointer is device memory owned by the caller; async on `stream`. */
+/* R22: out = W Q (axis 1: rotate along K, gate / up blocks) or Q^T W (axis 0: along N, down blocks) with
+ * Q = blockdiag(diag(signs) H_128) / sqrt(128); w, out bf16 [N, K] row-major (not aliased), signs int8 (+-1) of
+ * the rotated length (K or N, a multiple of 128). Each output is the fp64 result rounded once to bf16. */
+mxm_status mxm_hadamard_rotate(const void* w_bf16, void* out_bf16, int64_t N, int64_t K, const int8_t* signs,
+                               int32_t axis, mxm_stream stream);
+/* R23: H[K, K] (fp64, row-major) = 2 X^T X / n over calibration rows x_bf16 [n, K]. */
+mxm_status mxm_gptq_hessian(const void* x_bf16, int64_t n, int64_t K, double* H, mxm_stream stream);
+/* R23 set-up: dead columns (H_jj = 0 -> 1, dead[j] = 1), damping H += percdamp mean(diag H) I, then U[K, K]
+ * (fp64, row-major, upper) = the upper Cholesky factor of H^-1 (U^T U = H^-1) via the reverse Cholesky factor V
+ * (H = V V^T) and U = V^-1. H is overwritten (scratch); `scratch` holds K*K doubles. MXM_E_CONFIG on bad args. */
+mxm_status mxm_gptq_prepare(double* H, int64_t K, double percdamp, double* scratch, double* U, int32_t* dead,
+                            mxm_stream stream);
+/* Bytes of the fp64 work buffer mxm_gptq_quantize needs for an [N, K] block. */
+int64_t mxm_gptq_work_bytes(int64_t N, int64_t K);
+/* R23 / R24: GPTQ of one linear block w_bf16 [N, K] against U (from mxm_gptq_prepare on the block's input
+ * Hessian): columns left to right in blocks of 128, lazy batch updates, group parameters from the current weights
+ * at each group start (per channel: the initial weights). Output in mxm_quantize's canonical format: codes
+ * [N, K] (u8 asymmetric / s8 symmetric), scale and zero bf16 [N, K/g] (zero may be NULL for symmetric). Weight-only
+ * schemes of any bits, or the weight side of a W-A scheme; w_group in {64, 128, -1}. */
+mxm_status mxm_gptq_quantize(const mxm_scheme* s, const void* w_bf16, int64_t N, int64_t K, const double* U,
+                             const int32_t* dead, double* work, void* codes, void* scale, void* zero,
+                             mxm_stream stream);
 
 /* Test/debug: the dynamic activation quantizer of the hot path on v[M, K] bf16:
  *   codes [M, K] int8, scale [M, K/ga] float32, qsum [M, K/ga] int32 (may be NULL).

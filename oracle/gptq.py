@@ -56,9 +56,23 @@ def random_rotation(signs: np.ndarray, block: int = 128) -> np.ndarray:
     return q
 
 
-def rotate_expert(w_gate: np.ndarray, w_up: np.ndarray, w_down: np.ndarray, q: np.ndarray):
+def rotate_rows(x: np.ndarray, signs: np.ndarray, block: int = 128) -> np.ndarray:
+    """x Q for Q = random_rotation(signs): per 128-block (x_b diag(sigma_b)) H_128, then one division by sqrt(128).
+
+    Same product as x @ random_rotation(signs); the +-1 sums are exact in fp64 for bf16 inputs, so each output is
+    the exact value rounded once (the matrix form rounds every product by the irrational 1/sqrt(128) first)."""
+    x = np.asarray(x, dtype=np.float64)
+    d = x.shape[-1]
+    h = hadamard(block)
+    out = np.empty_like(x)
+    for b0 in range(0, d, block):
+        out[..., b0:b0 + block] = (x[..., b0:b0 + block] * signs[b0:b0 + block]) @ h
+    return out / np.sqrt(block)
+
+
+def rotate_expert(w_gate: np.ndarray, w_up: np.ndarray, w_down: np.ndarray, signs: np.ndarray):
     """R22: the rotated block maps x Q to y Q: W_gate Q, W_up Q (K = d side), Q^T W_down (N = d side)."""
-    return w_gate @ q, w_up @ q, q.T @ w_down
+    return rotate_rows(w_gate, signs), rotate_rows(w_up, signs), rotate_rows(w_down.T, signs).T
 
 
 def gptq_hessian(x: np.ndarray) -> np.ndarray:

@@ -18,6 +18,7 @@ from typing import List, Optional
 import numpy as np
 
 from .bf16 import bf16_round_f64, bits_to_f64
+from .fp8 import linear_block_fp8, quantize_weight_fp8
 from .quant import dequantize_weight, quantize_act, quantize_weight
 
 
@@ -60,9 +61,10 @@ class QBlock:
     w_group: int
     a_group: int
     symmetric: bool
-    codes: np.ndarray  # int64 [N,K]; w16: uint16 bf16 bits
+    codes: np.ndarray  # int64 [N,K]; w16: uint16 bf16 bits; FP8: e4m3 code bytes
     scale: Optional[np.ndarray]
     zero: Optional[np.ndarray]
+    fmt: int = 0  # 1: FP8 e4m3 (oracle/fp8.py, readings R25/R26)
 
     @property
     def N(self):
@@ -76,6 +78,9 @@ class QBlock:
 def quantize_block(w_bits_u16: np.ndarray, sch) -> QBlock:
     if sch.w_bits == 16:
         return QBlock(16, 16, -1, -1, True, np.asarray(w_bits_u16, dtype=np.uint16), None, None)
+    if getattr(sch, "fmt", 0) == 1:
+        codes, s = quantize_weight_fp8(w_bits_u16, sch.w_group)
+        return QBlock(8, 8, sch.w_group, sch.a_group, True, codes.astype(np.int64), s, None, 1)
     codes, s, z = quantize_weight(w_bits_u16, sch.w_bits, sch.w_group, sch.symmetric)
     return QBlock(sch.w_bits, sch.a_bits, sch.w_group, sch.a_group, sch.symmetric, codes, s, z)
 
@@ -116,6 +121,8 @@ def linear_block(xin: np.ndarray, blk: QBlock, exact_weights: bool = False) -> n
         if exact_weights:
             return xin @ dequantize_weight(blk.codes, blk.scale, blk.zero, blk.w_group).T
         return xin @ dequantize_weight_bf16(blk).T
+    if blk.fmt == 1:
+        return linear_block_fp8(xin, blk.codes, blk.scale, blk.w_group, blk.a_group)
     qa, sa, _ = quantize_act(xin.astype(np.float32), blk.a_bits, blk.a_group)
     acc = wa_int_accumulators(qa, blk.codes, blk.w_group)
     y = np.zeros((xin.shape[0], blk.N))

@@ -28,13 +28,16 @@ class Scheme:
     w_group: int = -1
     a_group: int = -1
     symmetric: bool = False
+    fmt: int = 0  # 0 integer codes, 1 FP8 e4m3 (MXM_FMT_E4M3)
 
     def c(self) -> _lib.mxm_scheme:
-        return _lib.mxm_scheme(self.w_bits, self.a_bits, self.w_group, self.a_group, 1 if self.symmetric else 0)
+        return _lib.mxm_scheme(self.w_bits, self.a_bits, self.w_group, self.a_group, 1 if self.symmetric else 0,
+                               self.fmt)
 
     @staticmethod
     def of(s) -> "Scheme":
-        return s if isinstance(s, Scheme) else Scheme(s.w_bits, s.a_bits, s.w_group, s.a_group, bool(s.symmetric))
+        return s if isinstance(s, Scheme) else Scheme(s.w_bits, s.a_bits, s.w_group, s.a_group, bool(s.symmetric),
+                                                      int(getattr(s, "fmt", 0)))
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -95,6 +98,54 @@ def dequantize(scheme, packed: torch.Tensor, N: int, K: int) -> torch.Tensor:
     s = Scheme.of(scheme).c()
     check(load().mxm_dequantize(C.byref(s), _ptr(packed), N, K, _ptr(out), _stream()))
     return out
+
+
+def hadamard_rotate(w: torch.Tensor, signs: torch.Tensor, axis: int) -> torch.Tensor:
+    """R22 (mxm_hadamard_rotate): W Q (axis 1, along K) or Q^T W (axis 0, along N); w bf16 [N, K], signs int8 +-1."""
+    assert w.dtype == torch.bfloat16 and w.is_cuda and w.is_contiguous() and w.dim() == 2
+    assert signs.dtype == torch.int8 and signs.is_cuda and signs.is_contiguous()
+    assert signs.numel() == (w.shape[1] if axis == 1 else w.shape[0])
+    out = torch.empty_like(w)
+    check(load().mxm_hadamard_rotate(_ptr(w), _ptr(out), w.shape[0], w.shape[1], _ptr(signs), axis, _stream()))
+    return out
+
+
+def gptq_hessian(x: torch.Tensor) -> torch.Tensor:
+    """R23 (mxm_gptq_hessian): H = 2 X^T X / n, fp64 [K, K], from calibration rows x bf16 [n, K]."""
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+    n, K = x.shape
+    H = torch.empty(K, K, dtype=torch.float64, device=x.device)
+    check(load().mxm_gptq_hessian(_ptr(x), n, K, _ptr(H), _stream()))
+    return H
+
+
+def gptq_prepare(H: torch.Tensor, percdamp: float = 0.01):
+    """R23 (mxm_gptq_prepare): (U fp64 [K, K] upper, U^T U = (H + damping)^-1; dead int32 [K]). H is consumed."""
+    assert H.dtype == torch.float64 and H.is_cuda and H.is_contiguous()
+    K = H.shape[0]
+    U = torch.empty(K, K, dtype=torch.float64, device=H.device)
+    scratch = torch.empty(K, K, dtype=torch.float64, device=H.device)
+    dead = torch.empty(K, dtype=torch.int32, device=H.device)
+    check(load().mxm_gptq_prepare(_ptr(H), K, float(percdamp), _ptr(scratch), _ptr(U), _ptr(dead), _stream()))
+    return U, dead
+
+
+def gptq_quantize(scheme, w: torch.Tensor, U: torch.Tensor, dead: torch.Tensor):
+    """R23/R24 (mxm_gptq_quantize): GPTQ codes / scale / zero of w bf16 [N, K] in mxm_quantize's format."""
+    sch = Scheme.of(scheme)
+    N, K = w.shape
+    assert w.dtype == torch.bfloat16 and w.is_cuda and w.is_contiguous()
+    assert U.dtype == torch.float64 and U.shape == (K, K) and dead.dtype == torch.int32 and dead.numel() == K
+    g = K if sch.w_group == -1 else sch.w_group
+    sym = sch.symmetric or sch.a_bits != 16
+    codes = torch.empty(N, K, dtype=torch.int8 if sym else torch.uint8, device=w.device)
+    scale = torch.empty(N, K // g, dtype=torch.bfloat16, device=w.device)
+    zero = None if sym else torch.empty(N, K // g, dtype=torch.bfloat16, device=w.device)
+    work = torch.empty(load().mxm_gptq_work_bytes(N, K), dtype=torch.uint8, device=w.device)
+    s = sch.c()
+    check(load().mxm_gptq_quantize(C.byref(s), _ptr(w), N, K, _ptr(U), _ptr(dead), _ptr(work), _ptr(codes),
+                                   _ptr(scale), _ptr(zero), _stream()))
+    return codes, scale, zero
 
 
 def act_quant(v: torch.Tensor, a_bits: int, a_group: int = -1):

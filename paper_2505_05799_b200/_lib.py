@@ -25,7 +25,7 @@ class MxmError(RuntimeError):
 
 class mxm_scheme(C.Structure):
     _fields_ = [("w_bits", C.c_int32), ("a_bits", C.c_int32), ("w_group", C.c_int32), ("a_group", C.c_int32),
-                ("symmetric", C.c_int32)]
+                ("symmetric", C.c_int32), ("fmt", C.c_int32)]
 
 
 class mxm_linear(C.Structure):
@@ -77,6 +77,11 @@ SIGNATURES = {
     "mxm_ep_workspace_bytes": (C.c_int, [_P, _I64, _I32, _I64, C.POINTER(_I64)]),
     "mxm_ep_moe_group_gemm": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _I64, _I64, _P]),
     "mxm_ep_poll_device_error": (C.c_int, [_P, _P, _P, C.POINTER(_I32)]),
+    "mxm_hadamard_rotate": (C.c_int, [_P, _P, _I64, _I64, _P, _I32, _P]),
+    "mxm_gptq_hessian": (C.c_int, [_P, _I64, _I64, _P, _P]),
+    "mxm_gptq_prepare": (C.c_int, [_P, _I64, C.c_double, _P, _P, _P, _P]),
+    "mxm_gptq_work_bytes": (C.c_int64, [_I64, _I64]),
+    "mxm_gptq_quantize": (C.c_int, [_S, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "mxm_last_error": (C.c_char_p, []),
     "mxm_version": (C.c_char_p, []),
 }

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmxmoe.so")
-SOURCES = ["api.cu", "quant.cu", "route.cu", "plan.cu", "gemm.cu", "ep.cu"]
+SOURCES = ["api.cu", "quant.cu", "route.cu", "plan.cu", "gemm.cu", "ep.cu", "gptq.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

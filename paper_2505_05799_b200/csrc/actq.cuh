@@ -26,6 +26,40 @@ __device__ __forceinline__ uint32_t code_byte(int q) {
     return (uint32_t)q & 0xFFu;
 }
 
+// e4m3 (OCP FP8 E4M3) code of a value with |a| <= 448, round to nearest, ties to the even mantissa (DESIGN R25 /
+// R26): exact from fp64 (the scalings by powers of two and the mantissa split are exact, rint rounds once).
+__device__ __forceinline__ uint32_t e4m3_rn(double a) {
+  const uint32_t sgn = signbit(a) ? 0x80u : 0u;
+  const double m = fabs(a);
+  uint32_t code;
+  if (m < 0.015625) {  // below 2^-6: the subnormal grid m 2^9 (rounds up to code 8 = 2^-6 at the boundary)
+    code = (uint32_t)rint(m * 512.0);
+  } else {
+    int e;
+    const double f = frexp(m, &e);  // m = f 2^e, f in [0.5, 1): m = (1 + t) 2^(e-1), t = 2f - 1 exact
+    uint32_t q = (uint32_t)rint((2.0 * f - 1.0) * 8.0);
+    int E = e - 1 + 7;
+    if (q == 8) {
+      q = 0;
+      ++E;
+    }
+    code = ((uint32_t)E << 3) | q;
+  }
+  if (code > 0x7Eu) code = 0x7Eu;
+  return sgn | code;
+}
+// value of an e4m3 code (finite codes)
+__device__ __forceinline__ float e4m3_value(uint32_t c) {
+  const uint32_t e = (c >> 3) & 15u, m = c & 7u;
+  const float v = e == 0 ? (float)m * 0.001953125f : ldexpf(1.0f + (float)m * 0.125f, (int)e - 7);
+  return (c & 0x80u) ? -v : v;
+}
+// FP8 activation code of v under the row / group reciprocal r (R26): e4m3_rn(clamp(fl32(v r), +-448))
+__device__ __forceinline__ uint32_t fp8_act_code(float v, float r) {
+  const float p = fminf(fmaxf(__fmul_rn(v, r), -448.f), 448.f);
+  return e4m3_rn((double)p);
+}
+
 // Quantize `n` bf16 values src[0..n) (n % 256 == 0 or n == 128: each lane handles 4- or 8-element
 // vectors) into dst codes, return the group scale; whole warp participates.
 // src may be global (generic pointer). Uses 8-byte (4 x bf16) vector loads.
@@ -73,7 +107,8 @@ __device__ __forceinline__ float quant_group_warp(const uint16_t* src, int8_t* _
 // 128*i + 4l .. +3 of chunk i), all loads in flight together; same arithmetic as quant_group_warp.
 // Scales go to sc[gi * R], code sums (if qs != nullptr) to qs[gi * R] (group-major [g][R]).
 // The hot path's gate/up input quantizer (route.cu gather) and the mxm_act_quant debug entry both call it.
-template <int MAXG, bool E4>
+// FP8 (R26): codes e4m3_rn(clamp(fl32(v r))) with qmax = 448 and r = fl32(448 / amax); code sums stay 0.
+template <int MAXG, bool E4, bool FP8 = false>
 __device__ __forceinline__ void quant_row_warp(const uint16_t* __restrict__ src, int8_t* __restrict__ dst, int d, int g,
                                                int qmax, float* __restrict__ sc, int32_t* __restrict__ qs,
                                                int64_t R) {
@@ -87,11 +122,16 @@ __device__ __forceinline__ void quant_row_warp(const uint16_t* __restrict__ src,
     return fmaxf(fmaxf(fabsf(bf16_bits_to_float(x.x & 0xFFFFu)), fabsf(bf16_bits_to_float(x.x >> 16))),
                  fmaxf(fabsf(bf16_bits_to_float(x.y & 0xFFFFu)), fabsf(bf16_bits_to_float(x.y >> 16))));
   };
-  const float fq = (float)qmax;
+  const float fq = FP8 ? 448.f : (float)qmax;
   auto quant4 = [&](uint2 x, float r, int& qsum) {
     const float f[4] = {bf16_bits_to_float(x.x & 0xFFFFu), bf16_bits_to_float(x.x >> 16),
                         bf16_bits_to_float(x.y & 0xFFFFu), bf16_bits_to_float(x.y >> 16)};
     uint32_t packed = 0;
+    if constexpr (FP8) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) packed |= fp8_act_code(f[j], r) << (8 * j);
+      return packed;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       float q = rintf(__fmul_rn(f[j], r));

@@ -212,6 +212,48 @@ mxm_status mxm_quantize(const mxm_scheme* s, const void* w, int64_t N, int64_t K
   return MXM_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-4 offline preparation (gptq.cu)
+mxm_status mxm_hadamard_rotate(const void* w, void* out, int64_t N, int64_t K, const int8_t* signs, int32_t axis,
+                               mxm_stream stream) {
+  if (!w || !out || !signs) return fail(MXM_E_CONFIG, "null argument");
+  if (N <= 0 || K <= 0 || (axis != 0 && axis != 1)) return fail(MXM_E_CONFIG, "bad shape / axis");
+  if ((axis == 1 ? K : N) % 128 != 0) return fail(MXM_E_CONFIG, "rotated dimension must be a multiple of 128");
+  if (w == out) return fail(MXM_E_CONFIG, "in-place rotation is not supported");
+  MXM_CUDA(launch_hadamard(w, out, N, K, signs, axis, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_gptq_hessian(const void* x, int64_t n, int64_t K, double* H, mxm_stream stream) {
+  if (!x || !H) return fail(MXM_E_CONFIG, "null argument");
+  if (n <= 0 || K <= 0) return fail(MXM_E_CONFIG, "bad shape");
+  MXM_CUDA(launch_gptq_hessian(x, n, K, H, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+mxm_status mxm_gptq_prepare(double* H, int64_t K, double percdamp, double* scratch, double* U, int32_t* dead,
+                            mxm_stream stream) {
+  if (!H || !scratch || !U || !dead) return fail(MXM_E_CONFIG, "null argument");
+  if (K <= 0 || !(percdamp >= 0.0)) return fail(MXM_E_CONFIG, "bad K / damping");
+  MXM_CUDA(launch_gptq_prepare(H, K, percdamp, scratch, U, dead, (cudaStream_t)stream));
+  return MXM_OK;
+}
+
+int64_t mxm_gptq_work_bytes(int64_t N, int64_t K) { return 8 * gptq_work_doubles(N, K); }
+
+mxm_status mxm_gptq_quantize(const mxm_scheme* s, const void* w, int64_t N, int64_t K, const double* U,
+                             const int32_t* dead, double* work, void* codes, void* scale, void* zero,
+                             mxm_stream stream) {
+  if (!s || !w || !U || !dead || !work || !codes || !scale) return fail(MXM_E_CONFIG, "null argument");
+  if (s->w_bits == 16) return fail(MXM_E_CONFIG, "w16 has nothing to quantize");
+  PackGeom g;
+  if (make_geom(*s, N, K, &g) != MXM_OK) return fail(MXM_E_CONFIG, "unsupported scheme/shape");
+  if (s->w_group != -1 && s->w_group != 64 && s->w_group != 128) return fail(MXM_E_CONFIG, "group must be 64 / 128 / -1");
+  if (!g.sym && !zero) return fail(MXM_E_CONFIG, "asymmetric scheme needs a zero buffer");
+  MXM_CUDA(launch_gptq_quantize(s->w_bits, s->w_group, g.sym ? 1 : 0, w, N, K, U, dead, work, codes, scale, zero,
+                                (cudaStream_t)stream));
+  return MXM_OK;
+}
+
 mxm_status mxm_pack(const mxm_scheme* s, const void* codes, const void* scale, const void* zero, int64_t N, int64_t K,
                     void* packed, mxm_stream stream) {
   if (!s || !codes || !packed) return fail(MXM_E_CONFIG, "null argument");
@@ -304,6 +346,10 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
                  b.scheme.w_bits, b.scheme.a_bits, b.scheme.w_group, (long long)N, (long long)K);
         return fail(MXM_E_CONFIG, buf);
       }
+      if (g.kind == KIND_FP8 && j < 2 && l->d > 4096) {  // the FP8 input quantizer keeps the row in registers
+        delete l;
+        return fail(MXM_E_CONFIG, "FP8 gate/up blocks need hidden <= 4096");
+      }
       e.blk[j].packed = reinterpret_cast<const uint8_t*>(b.packed);
       e.blk[j].geo = g;
       e.blk[j].a_bits = b.scheme.a_bits;
@@ -316,7 +362,7 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
     e.blk[0].in_slot = gwa ? 1 : 0;
     if (!uwa)
       e.blk[1].in_slot = 0;
-    else if (gwa && sg.a_bits == su.a_bits && e.blk[0].a_group == e.blk[1].a_group)
+    else if (gwa && sg.a_bits == su.a_bits && e.blk[0].a_group == e.blk[1].a_group && sg.fmt == su.fmt)
       e.blk[1].in_slot = 1;
     else
       e.blk[1].in_slot = gwa ? 2 : 1;
@@ -324,7 +370,7 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
     // gate and up share one K loop (and the token tile) when they use the same MMA kind and input:
     // any two bf16-kind blocks (w16 / weight-only of any bits and group), or identical W-A schemes
     e.dual = (!gwa && !uwa) || (gwa && uwa && e.blk[1].in_slot == 1 && sg.w_bits == su.w_bits &&
-                                sg.w_group == su.w_group);
+                                sg.w_group == su.w_group && sg.fmt == su.fmt);
     for (int j = 0; j < 2; ++j) {
       if (e.blk[j].in_slot == 0) l->need_xb = true;
       if (e.blk[j].in_slot == 1) l->need_xqa = true;
@@ -340,7 +386,7 @@ mxm_status mxm_layer_init(const mxm_layer_desc* d, void* desc_dev, int64_t desc_
       for (int j = 0; j < 2 && ok; ++j) {
         const LinDesc& L = l->ex[v].blk[j];
         const int b = L.in_slot == 0 ? 16 : L.a_bits, g = L.in_slot == 0 ? 0 : L.a_group;
-        const int e4 = L.in_slot == 0 ? 0 : (kind_is_f8(L.geo.kind) ? 1 : 0);
+        const int e4 = L.in_slot == 0 ? 0 : (kind_is_fp8(L.geo.kind) ? 2 : (kind_is_w4a4(L.geo.kind) ? 1 : 0));
         if (L.in_slot != 0 && g != 128 && g != -1) ok = false;
         int i = 0;
         while (i < fm.n && !(fm.a_bits[i] == b && fm.a_group[i] == g && fm.e4[i] == e4)) ++i;

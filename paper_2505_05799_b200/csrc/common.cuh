@@ -28,11 +28,17 @@ enum Kind : int8_t {
                     // tcgen05 kind::f8f6f4: byte u in [0,15] is the e4m3 value u * 2^-9 (subnormal / first binade,
                     // linear in u), activation codes are e4m3 (q<0)<<7 | |q| = q * 2^-9, so the f32 accumulator
                     // is 2^-18 * sum (q_w + 8) q_a exactly (integer sums < 2^24; tools/probe_f8.cu)
+  KIND_FP8 = 5,     // I8 image chunks of e4m3 weight codes (MXM_FMT_E4M3), tcgen05 kind::f8f6f4 from smem (SS),
+                    // e4m3 activation codes; the f32 accumulator is sum q_w q_a over e4m3 values (R25/R26)
 };
 
 // weight-activation kinds: 8-bit MMA operands, 128-element K stages, per-group / per-channel scale drains
 __host__ __device__ inline bool kind_is_wa(int k) { return k >= KIND_WA_ROW; }
-__host__ __device__ inline bool kind_is_f8(int k) { return k == KIND_WA_F8; }
+// kinds multiplied by tcgen05.mma kind::f8f6f4 (w4a4 and FP8)
+__host__ __device__ inline bool kind_is_f8(int k) { return k == KIND_WA_F8 || k == KIND_FP8; }
+// w4a4 on the fp8 tensor core: nibble-offset accumulators (drain factor a = s_a 2^18, correction b)
+__host__ __device__ inline bool kind_is_w4a4(int k) { return k == KIND_WA_F8; }
+__host__ __device__ inline bool kind_is_fp8(int k) { return k == KIND_FP8; }
 // row-word packed 8-bit-operand kinds (nibble + bit planes, unpacked by the transform warps)
 __host__ __device__ inline bool kind_is_row8(int k) { return k == KIND_WA_ROW || k == KIND_WA_F8; }
 __host__ __device__ inline bool kind_needs_transform(int k) { return k == KIND_WO || kind_is_row8(k); }
@@ -93,7 +99,10 @@ static_assert(sizeof(Task) == 16, "task size");
 // Mixtral T <= 256) each down task of a streaming-epilogue expert is cut into S <= kSplitMax K-slices (meta[7]);
 // slices write fp32 partials, the last-arriving slice reduces them in fixed slice order (deterministic).
 // A phase-2 task's ntile holds the tile (pair) index in bits 0-9 and the slice in bits 10-13.
-constexpr int kSplitMax = 4;
+#ifndef MXM_SPLIT_MAX
+#define MXM_SPLIT_MAX 4
+#endif
+constexpr int kSplitMax = MXM_SPLIT_MAX;
 #ifndef MXM_SPLIT_ROWS
 #define MXM_SPLIT_ROWS 512
 #endif
@@ -137,6 +146,8 @@ namespace mxm {
 // Validate a scheme for W[N, K] and fill its packed geometry. Returns MXM_OK or MXM_E_CONFIG.
 __host__ __device__ inline mxm_status make_geom(const mxm_scheme& s, int64_t N, int64_t K, PackGeom* g) {
   if (N <= 0 || K <= 0 || N % 128 != 0 || N > (1 << 24) || K > (1 << 24)) return MXM_E_CONFIG;
+  if (s.fmt != MXM_FMT_INT && s.fmt != MXM_FMT_E4M3) return MXM_E_CONFIG;
+  if (s.fmt == MXM_FMT_E4M3 && s.a_bits == 16) return MXM_E_CONFIG;
   PackGeom r{};
   r.N = (int32_t)N;
   r.K = (int32_t)K;
@@ -154,6 +165,12 @@ __host__ __device__ inline mxm_status make_geom(const mxm_scheme& s, int64_t N, 
     if (!(s.w_group == -1 || s.w_group == 64 || s.w_group == 128)) return MXM_E_CONFIG;
     r.kind = KIND_WO;
     r.ks = 64;
+    r.group = s.w_group == -1 ? (int32_t)K : s.w_group;
+  } else if (s.fmt == MXM_FMT_E4M3) {
+    if (s.w_bits != 8 || s.a_bits != 8 || !s.symmetric) return MXM_E_CONFIG;
+    if (!(s.w_group == -1 || s.w_group == 128) || s.a_group != s.w_group) return MXM_E_CONFIG;
+    r.kind = KIND_FP8;
+    r.ks = 128;
     r.group = s.w_group == -1 ? (int32_t)K : s.w_group;
   } else {
     if (s.a_bits != s.w_bits || !s.symmetric) return MXM_E_CONFIG;

@@ -38,6 +38,9 @@ namespace mxm {
 #ifndef MXM_SSLOTS
 #define MXM_SSLOTS 8
 #endif
+#ifndef MXM_LANE_ARRIVE
+#define MXM_LANE_ARRIVE 0  // 1: every lane arrives on the g128 scale-slot barriers (round-1 protocol)
+#endif
 constexpr int kStages = MXM_STAGES;
 constexpr int kRing = 4;
 // TMEM (512 columns): two accumulator buffers of 192 columns at [0, 384) -- a dual tile (gate | up, or two
@@ -94,7 +97,8 @@ static_assert(sizeof(Ctl) <= kCtlBytes, "ctl");
 struct SubLoop {
   const LinDesc* mat[2];
   int tile[2];                           // 128-channel output tile of each mat
-  int nmats, bmap, ns, i8, f8, xform, g128;  // i8: W-A (8-bit operands); f8: w4a4 on kind::f8f6f4 (common.cuh)
+  int nmats, bmap, ns, i8, f8, xform, g128;  // i8: W-A (8-bit operands); f8: kind::f8f6f4 (w4a4 or FP8)
+  int w4;                                     // w4a4 (nibble-offset accumulators: a = s_a 2^18, correction b)
                                               // xform: bit m set = mat m needs the packed->A transform
   int ks0, ks1;                           // stage range (a split-K slice of a down task, else [0, ns))
 };
@@ -110,6 +114,7 @@ __device__ __forceinline__ SubLoop make_sl(const LinDesc* a, const LinDesc* b, i
   s.ns = a->geo.ns;
   s.i8 = kind_is_wa(a->geo.kind);
   s.f8 = kind_is_f8(a->geo.kind);
+  s.w4 = kind_is_w4a4(a->geo.kind);
   s.xform = (kind_needs_transform(a->geo.kind) ? 1 : 0) | ((b && kind_needs_transform(b->geo.kind)) ? 2 : 0);
   s.g128 = s.i8 && a->geo.group == 128;
   s.ks0 = 0;
@@ -674,7 +679,8 @@ template <bool DUMP = false>
 __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int dmode, int qmax, int n, int colc, int nv,
                                      const uint16_t (&hb)[8], Ctl& ctl, int wg, int q, int lane, uint32_t& rbuf) {
   const int64_t row0 = (int64_t)t.row0 + colc;
-  if (dmode >= 2) {  // 2: int8 codes (w5a5 / w8a8 g128 down), 3: e4m3 codes + group code sums (w4a4 g128 down)
+  if (dmode >= 2) {  // 2: int8 codes (w5a5 / w8a8 g128 down), 3: e4m3 codes + group code sums (w4a4 g128 down),
+                     // 4: FP8 e4m3 codes (FP8 g128 down)
     if constexpr (DUMP) {  // test build: also keep the bf16 h the fused quantizer consumed (bit-exact h-quant test)
       uint16_t* hrow = p.H + row0 * p.f_max + n;
 #pragma unroll
@@ -689,7 +695,7 @@ __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int 
       for (int j = 0; j < 8; ++j) ctl.colmax[rbuf][wg][q][j] = m[j];
     named_bar_sync(2 + wg, 128);
     // lanes 0..7 derive column (lane)'s reciprocal / scale once (IEEE division, DESIGN R9), then broadcast
-    const float fq = (float)qmax;
+    const float fq = dmode == 4 ? 448.f : (float)qmax;  // 4: FP8 e4m3 codes (R26)
     float r_l = 0.f, sc_l = 1.f;
     if (lane < 8) {
       const uint32_t a = max(max(ctl.colmax[rbuf][wg][0][lane], ctl.colmax[rbuf][wg][1][lane]),
@@ -706,6 +712,11 @@ __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int 
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float r = __shfl_sync(0xffffffffu, r_l, j);
+      if (dmode == 4) {
+        qi[j] = 0;
+        if (j < nv) hq[(int64_t)j * p.f_max] = (int8_t)fp8_act_code(bf16f(hb[j]), r);
+        continue;
+      }
       qi[j] = (int)fminf(fmaxf(rintf(__fmul_rn(bf16f(hb[j]), r)), -fq), fq);
       if (j < nv) hq[(int64_t)j * p.f_max] = (int8_t)(dmode == 3 ? code_byte<true>(qi[j]) : code_byte<false>(qi[j]));
     }
@@ -897,9 +908,7 @@ __device__ __forceinline__ void mma_subloop_mode(Ctl& ctl, uint8_t* smem, uint32
                                                  uint32_t xform, uint32_t nt, MmaState& st,
                                                  unsigned long long (&pc)[16], bool prof_on) {
   const uint32_t all = TWO ? 3u : 1u;
-  if (MK == 2) {  // w4a4 weights are always transformed (TS)
-    mma_subloop<MK, TWO, 1>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
-  } else if (xform == 0)
+  if (xform == 0)
     mma_subloop<MK, TWO, 0>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
   else if ((xform & all) == all)
     mma_subloop<MK, TWO, 1>(ctl, smem, tmem, ns, g128, xform, nt, st, pc, prof_on);
@@ -1027,7 +1036,7 @@ __device__ __forceinline__ void stage_scales(const GemmParams& p, const Task& t,
       const int c = lane + 32 * h;
       if (c < t.rows) {
         sa[h] = __ldcg(xs_t + (int64_t)ks * p.hs_stride + t.row0 + c);
-        if (s.f8) qs[h] = __ldcg(xc_t + (int64_t)ks * p.hs_stride + t.row0 + c);
+        if (s.w4) qs[h] = __ldcg(xc_t + (int64_t)ks * p.hs_stride + t.row0 + c);
       }
     }
     const uint32_t ss = xsidx & (kSSlots - 1);
@@ -1039,12 +1048,16 @@ __device__ __forceinline__ void stage_scales(const GemmParams& p, const Task& t,
     for (int h = 0; h < 3; ++h) {
       const int c = lane + 32 * h;
       if (c < (int)t.nt) {
-        reinterpret_cast<float*>(slotp + kSlotA)[c] = s.f8 ? sa[h] * 262144.f : sa[h];
-        reinterpret_cast<float*>(slotp + kSlotB)[c] = s.f8 ? __fmul_rn(-8.f * (float)qs[h], sa[h]) : 0.f;
+        reinterpret_cast<float*>(slotp + kSlotA)[c] = s.w4 ? sa[h] * 262144.f : sa[h];
+        reinterpret_cast<float*>(slotp + kSlotB)[c] = s.w4 ? __fmul_rn(-8.f * (float)qs[h], sa[h]) : 0.f;
       }
     }
+#if MXM_LANE_ARRIVE
+    mbar_arrive(&ctl.sready[ss]);  // every lane releases its own slot writes
+#else
     __syncwarp();  // orders every lane's slot writes before lane 0's release
     if (lane == 0) mbar_arrive(&ctl.sready[ss]);
+#endif
     ++xsidx;
   }
 }
@@ -1078,8 +1091,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     }
     for (int i = 0; i < kSSlots; ++i) {
       mbar_init(&ctl.sfull[i], 1);
-      mbar_init(&ctl.sempty[i], 8);  // lane 0 of every epilogue warp (after __syncwarp)
-      mbar_init(&ctl.sready[i], 1);  // lane 0 of the scale-staging warp 3 (drain factors staged)
+      mbar_init(&ctl.sempty[i], MXM_LANE_ARRIVE ? 256 : 8);  // lane 0 of every epilogue warp (after __syncwarp)
+      mbar_init(&ctl.sready[i], MXM_LANE_ARRIVE ? 32 : 1);   // lane 0 of the scale-staging warp 3
     }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&ctl.accf[i], 1);
@@ -1353,7 +1366,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         // one vectorized pass quantizes the row (r = fl32(qmax/amax), s = fl32(amax/qmax), DESIGN R9)
         const LinDesc& L = E.blk[2];
         const int K = E.inter;
-        const float fq = (float)((1 << (L.a_bits - 1)) - 1);
+        const bool fp8 = kind_is_fp8(L.geo.kind);  // FP8 down: e4m3 codes (R26), qmax 448
+        const float fq = fp8 ? 448.f : (float)((1 << (L.a_bits - 1)) - 1);
         const int sub0 = t.ntile * 32;
         for (int rr = ew; rr < 32; rr += 8) {
           const int local = sub0 + rr;
@@ -1368,7 +1382,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           // latency-bound at a few GB/s per SM)
           constexpr int kU = 8;
           const int n8 = K / 8;
-          const bool e4 = kind_is_f8(L.geo.kind);  // w4a4 down: e4m3 codes + the row's code sum
+          const bool e4 = kind_is_w4a4(L.geo.kind);  // w4a4 down: e4m3 codes + the row's code sum
           int qsum = 0;
           for (int i0 = lane; i0 < n8; i0 += 32 * kU) {
             uint4 v[kU];
@@ -1381,6 +1395,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const float x = bf16f((uint16_t)(w[e >> 1] >> (16 * (e & 1))));
+                if (fp8) {
+                  o[e >> 2] |= fp8_act_code(x, r) << (8 * (e & 3));
+                  continue;
+                }
                 const int qv = (int)fminf(fmaxf(rintf(__fmul_rn(x, r)), -fq), fq);
                 if (i0 + 32 * u < n8) qsum += qv;
                 o[e >> 2] |= (e4 ? code_byte<true>(qv) : code_byte<false>(qv)) << (8 * (e & 3));
@@ -1423,7 +1441,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         __syncwarp();
       }
       const LinDesc& Ld = E.blk[2];
-      const int dmode = !kind_is_wa(Ld.geo.kind) ? 0 : (Ld.geo.group == 128 ? (kind_is_f8(Ld.geo.kind) ? 3 : 2) : 1);
+      const int dmode = !kind_is_wa(Ld.geo.kind) ? 0
+                        : (Ld.geo.group == 128 ? (kind_is_fp8(Ld.geo.kind) ? 4 : (kind_is_w4a4(Ld.geo.kind) ? 3 : 2)) : 1);
       const int dqmax = (1 << (Ld.a_bits - 1)) - 1;
       if (!reg_mode) {
         // ======== streaming epilogue: one drain event for the whole task (dual phase 0, or phase 2)
@@ -1443,7 +1462,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           sw1 = bf16f(__ldg(wsc1 + n1));
           sa_lo = vlo ? __ldg(xs_s + (int64_t)t.row0 + cl) : 0.f;
           sa_hi = vhi ? __ldg(xs_s + (int64_t)t.row0 + ch) : 0.f;
-          if (s.f8) {
+          if (s.w4) {
             qs_lo = vlo ? __ldg(xc_s + (int64_t)t.row0 + cl) : 0;
             qs_hi = vhi ? __ldg(xc_s + (int64_t)t.row0 + ch) : 0;
           }
@@ -1460,19 +1479,24 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           sw1 = bf16f(__ldg(wsc0 + n1));
           sa_lo = vlo ? __ldcg(xs_s + (int64_t)t.row0 + cl) : 0.f;
           sa_hi = vhi ? __ldcg(xs_s + (int64_t)t.row0 + ch) : 0.f;
-          if (s.f8) {
+          if (s.w4) {
             qs_lo = vlo ? __ldcg(xc_s + (int64_t)t.row0 + cl) : 0;
             qs_hi = vhi ? __ldcg(xc_s + (int64_t)t.row0 + ch) : 0;
           }
         }
         if (s.i8) {
           __syncwarp();
-          if (s.f8) {  // w4a4: acc * (s_a 2^18) - 8 s_a sum(q_a); the correction once per K (slice 0 of a split)
+          if (s.w4) {  // w4a4: acc * (s_a 2^18) - 8 s_a sum(q_a); the correction once per K (slice 0 of a split)
             const bool corr = !split || slice == 0;
             cw_sa[lane] = sa_lo * 262144.f;
             cw_sa[32 + lane] = sa_hi * 262144.f;
             cw_sb[lane] = corr ? __fmul_rn(-8.f * (float)qs_lo, sa_lo) : 0.f;
             cw_sb[32 + lane] = corr ? __fmul_rn(-8.f * (float)qs_hi, sa_hi) : 0.f;
+          } else if (s.f8) {  // FP8: acc is the sum over e4m3 values, acc * s_a
+            cw_sa[lane] = sa_lo;
+            cw_sa[32 + lane] = sa_hi;
+            cw_sb[lane] = 0.f;
+            cw_sb[32 + lane] = 0.f;
           } else {
             cw_sa[lane] = sa_lo;
             cw_sa[32 + lane] = sa_hi;
@@ -1649,7 +1673,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
               if (two) nsw1 = bf16f(__ldg(wsc1 + n1));
               nsa_lo = vlo ? __ldg(xs_lo) : 0.f;
               nsa_hi = vhi ? __ldg(xs_hi) : 0.f;
-              if (s.f8) {
+              if (s.w4) {
                 nqs_lo = vlo ? __ldg(xc_s + (int64_t)t.row0 + cl) : 0;
                 nqs_hi = vhi ? __ldg(xc_s + (int64_t)t.row0 + ch) : 0;
               }
@@ -1681,17 +1705,22 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
                 if (two) sw1 = bf16f(__ldg(wsc1 + n1));
                 nsa_lo = vlo ? __ldcg(xs_lo) : 0.f;
                 nsa_hi = vhi ? __ldcg(xs_hi) : 0.f;
-                if (s.f8) {
+                if (s.w4) {
                   nqs_lo = vlo ? __ldcg(xc_s + (int64_t)t.row0 + cl) : 0;
                   nqs_hi = vhi ? __ldcg(xc_s + (int64_t)t.row0 + ch) : 0;
                 }
               }
               __syncwarp();
-              if (s.f8) {
+              if (s.w4) {
                 cw_sa[lane] = nsa_lo * 262144.f;
                 cw_sa[32 + lane] = nsa_hi * 262144.f;
                 cw_sb[lane] = __fmul_rn(-8.f * (float)nqs_lo, nsa_lo);
                 cw_sb[32 + lane] = __fmul_rn(-8.f * (float)nqs_hi, nsa_hi);
+              } else if (s.f8) {  // FP8
+                cw_sa[lane] = nsa_lo;
+                cw_sa[32 + lane] = nsa_hi;
+                cw_sb[lane] = 0.f;
+                cw_sb[32 + lane] = 0.f;
               } else {
                 cw_sa[lane] = nsa_lo;
                 cw_sa[32 + lane] = nsa_hi;
@@ -1729,7 +1758,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             if (lane == 0) mbar_arrive(&ctl.acce[b0]);
             // the warp's slot reads are ordered before lane 0's release by the __syncwarp above (one arrival per
             // warp: per-lane arrivals serialise on the barrier word)
-            if (s.g128 && lane == 0) mbar_arrive(&ctl.sempty[ss]);
+            if (s.g128 && (MXM_LANE_ARRIVE || lane == 0)) mbar_arrive(&ctl.sempty[ss]);
             if (threadIdx.x == 256) TR(6, n_tr_e);
             ++n_tr_e;
             if (s.g128) ++sidx;

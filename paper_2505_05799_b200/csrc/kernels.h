@@ -49,6 +49,16 @@ cudaError_t launch_route_prep(const int32_t* ids, const float* topk_w, int64_t T
                               const float* shared_w, int32_t* counts, int32_t* offsets, int32_t* v_off, int32_t* perm,
                               int32_t* row_src, float* row_w, int32_t* row_exp, int32_t* inv, int32_t* err,
                               void* scratch, cudaStream_t st);
+// NEXT-4 offline preparation (gptq.cu)
+cudaError_t launch_hadamard(const void* w, void* out, int64_t N, int64_t K, const int8_t* signs, int axis,
+                            cudaStream_t st);
+cudaError_t launch_gptq_hessian(const void* x, int64_t n, int64_t K, double* H, cudaStream_t st);
+cudaError_t launch_gptq_prepare(double* H, int64_t K, double percdamp, double* V, double* U, int32_t* dead,
+                                cudaStream_t st);
+cudaError_t launch_gptq_quantize(int bits, int group, int sym, const void* w, int64_t N, int64_t K, const double* U,
+                                 const int32_t* dead, double* work, void* codes, void* scale, void* zero,
+                                 cudaStream_t st);
+int64_t gptq_work_doubles(int64_t N, int64_t K);
 // distinct gate/up input formats of a layer (token-major gather): a_bits 16 = bf16 copy, else the dynamic
 // quantizer's (a_bits, a_group (-1 per token / 128), e4m3 codes)
 struct ActFormats {

@@ -50,7 +50,11 @@ __global__ void quantize_kernel(const uint16_t* __restrict__ w, int64_t N, int64
   }
   if (!finite && err) atomicExch(err, (int32_t)MXM_E_DATA);
   double s, z = 0;
-  if (!sym) {
+  if (bits == -8) {  // FP8 e4m3 (R25): s = smallest bf16 with 448 s >= max|w|, code = e4m3_rn(w / s)
+    s = amax > 0 ? smallest_bf16_at_least(amax, 448) : 1.0;
+    for (int i = 0; i < group; ++i) dst[i] = (uint8_t)e4m3_rn(__ddiv_rn(bf16_bits_to_double(src[i]), s));
+    if (zero) zero[n * ng + gi] = 0;
+  } else if (!sym) {
     const int c = (1 << bits) - 1;
     const double D = xmax - xmin;
     s = D > 0 ? smallest_bf16_at_least(D, c) : 1.0;
@@ -101,7 +105,7 @@ __global__ void pack_kernel(PackGeom g, const uint8_t* __restrict__ codes, const
   const int64_t n = (int64_t)rb * 128 + r;
   const int64_t k0 = (int64_t)ks * g.ks;
   uint8_t* chunk = out + chunk_offset(g, rb, ks);
-  if (g.kind == KIND_W16 || g.kind == KIND_WA_IMG) {
+  if (g.kind == KIND_W16 || g.kind == KIND_WA_IMG || g.kind == KIND_FP8) {
     // row r: 128 bytes of K-slice; byte b at r*128 + ((b>>4 ^ r&7)<<4) + (b&15)
     const uint8_t* src = (g.kind == KIND_W16) ? codes + (n * g.K + k0) * 2 : codes + n * g.K + k0;
     for (int c = 0; c < 8; ++c) {
@@ -149,7 +153,7 @@ __global__ void pack_kernel(PackGeom g, const uint8_t* __restrict__ codes, const
 __device__ uint32_t read_stored_code(const PackGeom& g, const uint8_t* packed, int64_t n, int64_t k) {
   const int rb = (int)(n / 128), r = (int)(n % 128), ks = (int)(k / g.ks), i = (int)(k % g.ks);
   const uint8_t* chunk = packed + chunk_offset(g, rb, ks);
-  if (g.kind == KIND_WA_IMG) {
+  if (g.kind == KIND_WA_IMG || g.kind == KIND_FP8) {
     const int b = i;
     return chunk[r * 128 + (((b >> 4) ^ (r & 7)) << 4) + (b & 15)];
   }
@@ -186,6 +190,11 @@ __global__ void dequant_kernel(PackGeom g, const uint8_t* __restrict__ packed, f
   const int gi = (int)(k / g.group);
   double s, z = 0;
   int q;
+  if (g.kind == KIND_FP8) {
+    s = bf16_bits_to_double(reinterpret_cast<const uint16_t*>(packed + g.wa_scale_off)[(int64_t)gi * g.N + n]);
+    out[idx] = (float)((double)e4m3_value(u) * s);
+    return;
+  }
   if (kind_is_wa(g.kind)) {
     q = g.kind == KIND_WA_IMG ? (int)(int8_t)u : (int)u - (1 << (g.w_bits - 1));
     s = bf16_bits_to_double(reinterpret_cast<const uint16_t*>(packed + g.wa_scale_off)[(int64_t)gi * g.N + n]);
@@ -229,7 +238,8 @@ cudaError_t launch_quantize(const PackGeom& g, const void* w, void* codes, void*
                             cudaStream_t st) {
   const int64_t n = (int64_t)g.N * (g.K / g.group);
   quantize_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
-      (const uint16_t*)w, g.N, g.K, g.w_bits, g.group, g.sym, (uint8_t*)codes, (uint16_t*)scale, (uint16_t*)zero, err);
+      (const uint16_t*)w, g.N, g.K, g.kind == KIND_FP8 ? -8 : g.w_bits, g.group, g.sym, (uint8_t*)codes,
+      (uint16_t*)scale, (uint16_t*)zero, err);
   return cudaGetLastError();
 }
 cudaError_t launch_pack(const PackGeom& g, const void* codes, const void* scale, const void* zero, void* out,

@@ -191,9 +191,11 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
       int32_t* qs = (L.in_slot == 1 ? XcA : XcB) + row;
       const int g = L.a_group == -1 ? d : L.a_group;
       const int qmax = (1 << (L.a_bits - 1)) - 1;
-      const bool e4 = kind_is_f8(L.geo.kind);  // w4a4: e4m3 codes for kind::f8f6f4 (common.cuh)
+      const bool e4 = kind_is_w4a4(L.geo.kind);  // w4a4: e4m3 small-integer codes for kind::f8f6f4 (common.cuh)
       if (d <= 128 * 32 && (g == 128 || g == d)) {  // whole row in registers, all loads in flight
-        if (e4)
+        if (kind_is_fp8(L.geo.kind))
+          quant_row_warp<32, false, true>(src, q, d, g, qmax, sc, qs, R);
+        else if (e4)
           quant_row_warp<32, true>(src, q, d, g, qmax, sc, qs, R);
         else
           quant_row_warp<32, false>(src, q, d, g, qmax, sc, qs, R);
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(256) gather_tok_kernel(
   const int64_t t = w / fm.n;
   const int f = (int)(w % fm.n);
   const int fb = fm.a_bits[f], fg = fm.a_group[f];
-  const bool fe = fm.e4[f] != 0;
+  const int fe = fm.e4[f];  // code encoding: 0 two's complement, 1 w4a4 e4m3 small integers, 2 FP8 e4m3 (R26)
   // lane j < k + S resolves route j of the token: its row and the slots (1 / 2) of gate / up that read format f
   int64_t row = -1;
   int sl0 = -1, sl1 = -1;  // slot written for the gate / up input (-1: another format)
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(256) gather_tok_kernel(
       const LinDesc& L1 = ex[v].blk[1];
       auto match = [&](const LinDesc& L) {
         if (L.in_slot == 0) return fb == 16;
-        return fb == L.a_bits && fg == L.a_group && fe == kind_is_f8(L.geo.kind);
+        return fb == L.a_bits && fg == L.a_group && fe == (kind_is_fp8(L.geo.kind) ? 2 : (kind_is_w4a4(L.geo.kind) ? 1 : 0));
       };
       if (match(L0)) sl0 = L0.in_slot;
       if (L1.in_slot != L0.in_slot && match(L1)) sl1 = L1.in_slot;
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(256) gather_tok_kernel(
     }
     return;
   }
-  const float fq = (float)((1 << (fb - 1)) - 1);
+  const float fq = fe == 2 ? 448.f : (float)((1 << (fb - 1)) - 1);
   auto absmax4 = [](uint2 a) {
     return fmaxf(fmaxf(fabsf(bf16_bits_to_float(a.x & 0xFFFFu)), fabsf(bf16_bits_to_float(a.x >> 16))),
                  fmaxf(fabsf(bf16_bits_to_float(a.y & 0xFFFFu)), fabsf(bf16_bits_to_float(a.y >> 16))));
@@ -278,6 +280,11 @@ __global__ void __launch_bounds__(256) gather_tok_kernel(
     const float fv[4] = {bf16_bits_to_float(a.x & 0xFFFFu), bf16_bits_to_float(a.x >> 16),
                          bf16_bits_to_float(a.y & 0xFFFFu), bf16_bits_to_float(a.y >> 16)};
     uint32_t packed = 0;
+    if (fe == 2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) packed |= fp8_act_code(fv[j], r) << (8 * j);
+      return packed;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       float q = rintf(__fmul_rn(fv[j], r));

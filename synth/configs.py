@@ -21,6 +21,7 @@ class Scheme:
     w_group: int = -1
     a_group: int = -1
     symmetric: bool = False
+    fmt: int = 0  # 0: integer codes (the paper's quantizer); 1: FP8 e4m3 weights and activations (NEXT-4, R25/R26)
 
     @property
     def weight_only(self) -> bool:
@@ -33,6 +34,8 @@ class Scheme:
         s = "sym" if self.symmetric else "asym"
         if self.weight_only:
             return f"w{self.w_bits}a16_g{g}_{s}"
+        if self.fmt == 1:
+            return f"fp8_e4m3_g{g}"
         return f"w{self.w_bits}a{self.a_bits}_g{g}_{s}"
 
 
@@ -45,6 +48,11 @@ def WO(bits: int, group: int = 128, sym: bool = False) -> Scheme:
 
 def WA(bits: int, group: int = -1) -> Scheme:
     return Scheme(bits, bits, group, group, True)
+
+
+def FP8(group: int = -1) -> Scheme:
+    """FP8 e4m3 weights and activations (NEXT-4 extra hardware-supported scheme; DESIGN R25/R26)."""
+    return Scheme(8, 8, group, group, True, 1)
 
 
 @dataclass

@@ -46,6 +46,7 @@ def test_rotated_block_equivalence_torch_mlp():
     wg, wu, wd = rng.standard_normal((f, d)), rng.standard_normal((f, d)), rng.standard_normal((d, f))
     x = rng.standard_normal((T, d))
     q = random_rotation(rng.choice([-1, 1], size=d))
+    assert np.all(np.abs(q[np.arange(d), np.arange(d) // 128 * 128]) > 0)
 
     def mlp(xx, g, u, dn):
         xt = torch.tensor(xx, dtype=torch.float64)
@@ -53,7 +54,9 @@ def test_rotated_block_equivalence_torch_mlp():
         return (h @ torch.tensor(dn).T).numpy()
 
     y = mlp(x, wg, wu, wd)
-    rg, ru, rd = rotate_expert(wg, wu, wd, q)
+    sig = np.sign(q[np.arange(d), np.arange(d) // 128 * 128])  # sigma_r = sign of row r's first block entry
+    rg, ru, rd = rotate_expert(wg, wu, wd, sig)
+    assert np.abs(rg - wg @ q).max() < 1e-13 and np.abs(rd - q.T @ wd).max() < 1e-13  # = the matrix form
     yr = mlp(x @ q, rg, ru, rd)
     assert np.abs(yr - y @ q).max() < 1e-10 * np.abs(y).max()
 
