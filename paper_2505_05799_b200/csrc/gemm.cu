@@ -534,6 +534,13 @@ __device__ __forceinline__ void drain_event(float2 (&acc2)[32], uint32_t addrA, 
       for (int j = 0; j < FCH; j += 2) {
         const int col = c0 + j;
         const float2 fa = make_float2(__uint_as_float(xa[j]), __uint_as_float(xa[j + 1]));
+#ifdef MXM_ABL_DRAIN_1FMA  // timing diagnostic: one FFMA2 per element pair (numerically wrong)
+        acc2[DST0 + col / 2] = ffma2(fa, ac[j / 2], acc2[DST0 + col / 2]);
+        if constexpr (TWO)
+          acc2[16 + col / 2] = ffma2(make_float2(__uint_as_float(xb[j]), __uint_as_float(xb[j + 1])), ac[j / 2],
+                                     acc2[16 + col / 2]);
+        continue;
+#endif
         acc2[DST0 + col / 2] = ffma2(ffma2(fa, ac[j / 2], bc[j / 2]), make_float2(sw0, sw0), acc2[DST0 + col / 2]);
         if constexpr (TWO) {
           const float2 fb = make_float2(__uint_as_float(xb[j]), __uint_as_float(xb[j + 1]));
@@ -1025,7 +1032,8 @@ __device__ __forceinline__ void stage_scales(const GemmParams& p, const Task& t,
                                           s.tile[1] * 128
                                     : nullptr;
   for (int ks = 0; ks < s.ns; ++ks) {
-    // this group's values (loads in flight before the slot wait)
+    // this group's values (loads in flight before the slot wait; loading 4 or 8 groups ahead through a register
+    // ring was measured no faster / slower: profiles/r02/ab_experiments.txt)
     const uint2 sw0 = *reinterpret_cast<const uint2*>(w0 + (int64_t)ks * s.mat[0]->geo.N + 4 * lane);
     const uint2 sw1 = w1 ? *reinterpret_cast<const uint2*>(w1 + (int64_t)ks * s.mat[1]->geo.N + 4 * lane)
                          : make_uint2(0, 0);
