@@ -517,7 +517,7 @@ def main():
                 "config": {"workload": cfg.name, "tokens_per_gpu": T, "experts": f"{cfg.n_routed}+{cfg.n_shared}",
                            "hidden": cfg.hidden, "inter": cfg.inter, "top_k": k, "table": args.table,
                            "l2": "flushed before every timed step (256 MB memset, untimed)",
-                           "parallelism": (f"ep{ws} (NCCL all-to-all dispatch/combine, shared experts replicated)"
+                           "parallelism": (f"ep{ws} (sync-free NCCL all-to-all dispatch/combine at fixed capacity, shared experts replicated)"
                                            if use_ep else f"replicas x{ws}") if ws > 1 else "single GPU"},
                 "roofline": roofline, "per_expert_roofline": per_expert, "stage_ms": stage_ms,
                 "cpu_baseline": cpu, "e2e": e2e, "comparators": comparators, "gpu_launches": launches * K, "clocks": clocks,

@@ -280,6 +280,14 @@ mxm_status mxm_ep_workspace_bytes(const mxm_ep* ep, int64_t T, int32_t top_k, in
 mxm_status mxm_ep_moe_group_gemm(mxm_ep* ep, const void* x, int64_t T, int32_t top_k, const int32_t* topk_ids,
                                  const float* topk_w, const float* shared_w, void* y, void* workspace, int64_t ws_bytes,
                                  int64_t max_recv_rows, mxm_stream stream);
+/* [sync] dispatch mode of the handle (NEXT-1 step; default MXM_EP_V1 as above). MXM_EP_SYNC_FREE: no host
+ * synchronisation at all -- every rank reserves T rows per destination (a token goes to a rank at most once), the
+ * exchanges use fixed equal counts, rows no token fills carry expert id -1 (no route, skipped by the local layer),
+ * the shared experts' ids / unit weights are written by a kernel. Requires the same T on every rank and
+ * max_recv_rows >= world_size * T (else MXM_E_CONFIG). The valid rows reach the local layer in the same relative
+ * order as in v1, so y is bitwise identical; the padding travels over the links. MXM_E_CONFIG on a bad mode. */
+enum { MXM_EP_V1 = 0, MXM_EP_SYNC_FREE = 1 };
+mxm_status mxm_ep_set_mode(mxm_ep* ep, int32_t mode);
 /* [sync] read and clear the EP workspace's error word (bad expert ids in topk_ids -> MXM_E_DATA). */
 mxm_status mxm_ep_poll_device_error(const mxm_ep* ep, const void* workspace, mxm_stream stream, int32_t* code);
 

@@ -77,6 +77,7 @@ SIGNATURES = {
     "mxm_ep_workspace_bytes": (C.c_int, [_P, _I64, _I32, _I64, C.POINTER(_I64)]),
     "mxm_ep_moe_group_gemm": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _I64, _I64, _P]),
     "mxm_ep_poll_device_error": (C.c_int, [_P, _P, _P, C.POINTER(_I32)]),
+    "mxm_ep_set_mode": (C.c_int, [_P, _I32]),
     "mxm_hadamard_rotate": (C.c_int, [_P, _P, _I64, _I64, _P, _I32, _P]),
     "mxm_gptq_hessian": (C.c_int, [_P, _I64, _I64, _P, _P]),
     "mxm_gptq_prepare": (C.c_int, [_P, _I64, C.c_double, _P, _P, _P, _P]),

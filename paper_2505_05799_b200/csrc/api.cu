@@ -769,6 +769,7 @@ struct mxm_ep {
   mxm_layer* shared = nullptr;
   ncclComm_t comm = nullptr;
   int G = 1, rank = 0, E = 0;
+  int mode = MXM_EP_V1;  // MXM_EP_SYNC_FREE: fixed-capacity exchange, no host sync (mxm_ep_set_mode)
 };
 
 namespace {
@@ -779,7 +780,8 @@ struct EpLayout {
 EpLayout ep_layout(const mxm_ep* ep, int64_t T, int k, int64_t max_recv) {
   EpLayout w{};
   const int64_t G = ep->G, d = ep->local->d, S = ep->shared ? ep->shared->E : 0;
-  const int64_t max_send = T * (k < G ? k : G);
+  // v1 sends at most min(k, G) rows per token in total; sync-free reserves T rows for every destination
+  const int64_t max_send = ep->mode == MXM_EP_SYNC_FREE ? T * G : T * (k < G ? k : G);
   int64_t o = 0;
   auto take = [&](int64_t bytes) {
     const int64_t at = o;
@@ -864,6 +866,12 @@ mxm_status mxm_ep_workspace_bytes(const mxm_ep* ep, int64_t T, int32_t k, int64_
   return MXM_OK;
 }
 
+mxm_status mxm_ep_set_mode(mxm_ep* ep, int32_t mode) {
+  if (!ep || (mode != MXM_EP_V1 && mode != MXM_EP_SYNC_FREE)) return fail(MXM_E_CONFIG, "bad EP handle / mode");
+  ep->mode = mode;
+  return MXM_OK;
+}
+
 mxm_status mxm_ep_moe_group_gemm(mxm_ep* ep, const void* x, int64_t T, int32_t k, const int32_t* topk_ids,
                                  const float* topk_w, const float* shared_w, void* y, void* ws, int64_t ws_bytes,
                                  int64_t max_recv_rows, mxm_stream stream) {
@@ -878,6 +886,51 @@ mxm_status mxm_ep_moe_group_gemm(mxm_ep* ep, const void* x, int64_t T, int32_t k
   int32_t* dest_counts = (int32_t*)P(w.dest_counts);
   int32_t* recv_counts = (int32_t*)P(w.recv_counts);
   int32_t* pos = (int32_t*)P(w.pos);
+  if (ep->mode == MXM_EP_SYNC_FREE) {
+    // fixed capacity C = T rows per destination (a token goes to a rank at most once): equal-count exchanges, no
+    // host read of any count; rows no token fills carry expert id -1 (no route) and are skipped by the local layer
+    const int64_t C = T, R = (int64_t)G * T;
+    if (R > max_recv_rows) return fail(MXM_E_CONFIG, "sync-free EP needs max_recv_rows >= G * T");
+    int32_t* dest_off = (int32_t*)P(w.dest_off);
+    MXM_CUDA(launch_ep_route(topk_ids, T, k, ep->E, G, dest_counts, pos, (int32_t*)P(w.err), st));
+    MXM_CUDA(launch_ep_fill(dest_off, G, C, (int32_t*)P(w.sid), (float*)P(w.ones), T, S, st));
+    MXM_CUDA(cudaMemsetAsync(P(w.send_ids), 0xFF, 4 * R * k, st));  // -1: no route
+    MXM_CUDA(cudaMemsetAsync(P(w.send_w), 0, 4 * R * k, st));
+    MXM_CUDA(launch_ep_pack(x, T, d, topk_ids, topk_w, k, ep->E, G, pos, dest_off, P(w.send_x),
+                            (int32_t*)P(w.send_ids), (float*)P(w.send_w), (int32_t*)P(w.send_src), st));
+    MXM_NCCL(ncclGroupStart());
+    for (int r = 0; r < G; ++r) {
+      MXM_NCCL(ncclSend((uint16_t*)P(w.send_x) + r * C * d, (size_t)(C * d), ncclBfloat16, r, ep->comm, st));
+      MXM_NCCL(ncclSend((int32_t*)P(w.send_ids) + r * C * k, (size_t)(C * k), ncclInt32, r, ep->comm, st));
+      MXM_NCCL(ncclSend((float*)P(w.send_w) + r * C * k, (size_t)(C * k), ncclFloat32, r, ep->comm, st));
+      MXM_NCCL(ncclRecv((uint16_t*)P(w.recv_x) + r * C * d, (size_t)(C * d), ncclBfloat16, r, ep->comm, st));
+      MXM_NCCL(ncclRecv((int32_t*)P(w.recv_ids) + r * C * k, (size_t)(C * k), ncclInt32, r, ep->comm, st));
+      MXM_NCCL(ncclRecv((float*)P(w.recv_w) + r * C * k, (size_t)(C * k), ncclFloat32, r, ep->comm, st));
+    }
+    MXM_NCCL(ncclGroupEnd());
+    if (R > 0) {
+      mxm_status s = run_group_gemm(ep->local, P(w.recv_x), R, k, (const int32_t*)P(w.recv_ids),
+                                    (const float*)P(w.recv_w), nullptr, P(w.recv_y), P(w.ws_local),
+                                    w.ws_local_bytes, stream, nullptr);
+      if (s != MXM_OK) return s;
+    }
+    MXM_NCCL(ncclGroupStart());
+    for (int r = 0; r < G; ++r) {
+      MXM_NCCL(ncclSend((uint16_t*)P(w.recv_y) + r * C * d, (size_t)(C * d), ncclBfloat16, r, ep->comm, st));
+      MXM_NCCL(ncclRecv((uint16_t*)P(w.back) + r * C * d, (size_t)(C * d), ncclBfloat16, r, ep->comm, st));
+    }
+    MXM_NCCL(ncclGroupEnd());
+    void* y_sh = nullptr;
+    if (S > 0 && T > 0) {
+      y_sh = P(w.y_sh);
+      mxm_status s = run_group_gemm(ep->shared, x, T, S, (const int32_t*)P(w.sid),
+                                    shared_w ? shared_w : (const float*)P(w.ones), nullptr, y_sh, P(w.ws_shared),
+                                    w.ws_shared_bytes, stream, nullptr);
+      if (s != MXM_OK) return s;
+    }
+    if (T > 0) MXM_CUDA(launch_ep_combine(P(w.back), pos, dest_off, G, T, d, y_sh, y, st));
+    return MXM_OK;
+  }
   // 1. per-destination deduplicated counts and slots, exchanged
   MXM_CUDA(launch_ep_route(topk_ids, T, k, ep->E, G, dest_counts, pos, (int32_t*)P(w.err), st));
   MXM_NCCL(ncclGroupStart());

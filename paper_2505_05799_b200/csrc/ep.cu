@@ -131,6 +131,23 @@ cudaError_t launch_ep_pack(const void* x, int64_t T, int d, const int32_t* ids, 
                                                                         dest_off, (uint16_t*)sx, sids, sw, ssrc);
   return cudaGetLastError();
 }
+// sync-free EP constants on the device (no host staging): dest_off[r] = r * C, the shared experts' ids
+// sid[t, s] = s and unit weights
+__global__ void ep_fill_kernel(int32_t* __restrict__ dest_off, int G, int64_t C, int32_t* __restrict__ sid,
+                               float* __restrict__ ones, int64_t T, int S) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= G) dest_off[i] = (int32_t)(i * C);
+  if (i < T * S) {
+    sid[i] = (int32_t)(i % S);
+    ones[i] = 1.0f;
+  }
+}
+cudaError_t launch_ep_fill(int32_t* dest_off, int G, int64_t C, int32_t* sid, float* ones, int64_t T, int S,
+                           cudaStream_t st) {
+  const int64_t n = (T * S > G + 1) ? T * S : G + 1;
+  ep_fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dest_off, G, C, sid, ones, T, S);
+  return cudaGetLastError();
+}
 cudaError_t launch_ep_combine(const void* back, const int32_t* pos, const int32_t* dest_off, int G, int64_t T, int d,
                               const void* ysh, void* y, cudaStream_t st) {
   if (T == 0) return cudaSuccess;

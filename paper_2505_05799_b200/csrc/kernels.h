@@ -84,6 +84,8 @@ cudaError_t launch_ep_route(const int32_t* ids, int64_t T, int k, int E, int G, 
 cudaError_t launch_ep_pack(const void* x, int64_t T, int d, const int32_t* ids, const float* w, int k, int E, int G,
                            const int32_t* pos, const int32_t* dest_off, void* sx, int32_t* sids, float* sw,
                            int32_t* ssrc, cudaStream_t st);
+cudaError_t launch_ep_fill(int32_t* dest_off, int G, int64_t C, int32_t* sid, float* ones, int64_t T, int S,
+                           cudaStream_t st);
 cudaError_t launch_ep_combine(const void* back, const int32_t* pos, const int32_t* dest_off, int G, int64_t T, int d,
                               const void* ysh, void* y, cudaStream_t st);
 

@@ -108,8 +108,9 @@ def _worker(rank, world, port, out_path):
     lo = rank * epr
     local = QuantizedLayer(epr, 0, cfg.hidden, cfg.inter, 0, full.blocks[lo:lo + epr])
     shared = QuantizedLayer(cfg.n_shared, 0, cfg.hidden, cfg.shared_inter, 0, full.blocks[cfg.n_routed:])
-    ep = ExpertParallelMoE(cfg.n_routed, cfg.hidden, OracleLayer(local), OracleLayer(shared), cfg.n_shared,
-                           ops=TorchRefEpOps())
+    eps = {mode: ExpertParallelMoE(cfg.n_routed, cfg.hidden, OracleLayer(local), OracleLayer(shared), cfg.n_shared,
+                                   ops=TorchRefEpOps(), sync_free=mode == "sync_free")
+           for mode in ("v1", "sync_free")}
     # each rank owns a different slice of the tokens (data parallel), routing is global
     T = case["T"]
     sl = slice(rank * T // world, (rank + 1) * T // world)
@@ -117,8 +118,9 @@ def _worker(rank, world, port, out_path):
     ids = torch.from_numpy(case["ids"][sl].astype(np.int32))
     w = torch.from_numpy(case["w"][sl])
     sw = torch.from_numpy(case["shared_w"][sl])
-    y = ep(x, ids, w, sw)
-    np.save(f"{out_path}_{rank}.npy", y.float().numpy())
+    for mode, ep in eps.items():
+        y = ep(x, ids, w, sw)
+        np.save(f"{out_path}_{mode}_{rank}.npy", y.float().numpy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -135,7 +137,10 @@ def _free_port():
 def test_ep_two_ranks_equals_unsharded_oracle(tmp_path, world):
     out = str(tmp_path / "y")
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
-    y = np.concatenate([np.load(f"{out}_{r}.npy") for r in range(world)])
+    y = np.concatenate([np.load(f"{out}_v1_{r}.npy") for r in range(world)])
+    # the sync-free exchange (fixed capacity, padding rows without routes) gives the same bits as v1
+    y_sf = np.concatenate([np.load(f"{out}_sync_free_{r}.npy") for r in range(world)])
+    assert np.array_equal(y, y_sf)
     from oracle.moe import moe_block, quantize_layer
     from tests.moe_cases import row_rel_err
     cfg, table, case = _case()

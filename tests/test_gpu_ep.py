@@ -98,6 +98,26 @@ def test_ep_loopback_equals_unsharded(mx, G):
         ys.append(ops.combine(back.contiguous(), route[r][1], torch.tensor(offs[r], dtype=torch.int32).cuda(), G, ysh,
                               Tr, d))
     y = torch.cat(ys).float().cpu().numpy().astype(np.float64)
+    # sync-free exchange (ep.py): fixed capacity Tr rows per destination, padding rows with expert id -1;
+    # destination q receives G * Tr rows, the valid ones in the same relative order -> the same bits
+    cap = Tr
+    doff = torch.arange(G + 1, dtype=torch.int32, device="cuda") * cap
+    cpacks = [ops.pack(xs[r], ids[r], ws[r], route[r][1], doff, E, G, G * cap) for r in range(G)]
+    couts = {}
+    for q in range(G):
+        rx = torch.cat([cpacks[r][0][q * cap:(q + 1) * cap] for r in range(G)])
+        rid = torch.cat([cpacks[r][1][q * cap:(q + 1) * cap] for r in range(G)])
+        rw = torch.cat([cpacks[r][2][q * cap:(q + 1) * cap] for r in range(G)])
+        ry = locals_[q](rx.contiguous(), rid.contiguous(), rw.contiguous())
+        for r in range(G):
+            couts[(r, q)] = ry[r * cap:(r + 1) * cap]
+    ys2 = []
+    for r in range(G):
+        back = torch.cat([couts[(r, q)] for q in range(G)])
+        sid = torch.arange(S, dtype=torch.int32, device="cuda").repeat(Tr, 1)
+        ysh = shared(xs[r], sid, sws[r])
+        ys2.append(ops.combine(back.contiguous(), route[r][1], doff, G, ysh, Tr, d))
+    assert torch.equal(torch.cat(ys), torch.cat(ys2))
     rows = np.arange(0, T, 4)
     ref = oracle_run(oracle_layer(case), case, rows=rows)
     assert row_rel_err(y[rows], ref) <= 1e-2
@@ -127,10 +147,15 @@ def test_ep_c_abi_nccl_world1(mx):
     ids = torch.from_numpy(case["ids"]).cuda()
     w = torch.from_numpy(case["w"]).cuda()
     sw = torch.from_numpy(case["shared_w"]).cuda()
-    y_py = py(x, ids, w, sw)
-    y_c = cab(x, ids, w, sw)
+    y_py = py(x, ids, w, sw)  # torch orchestration, sync-free
+    py.sync_free = False
+    y_v1 = py(x, ids, w, sw)  # torch orchestration, v1
+    y_c = cab(x, ids, w, sw)  # C ABI, sync-free (default)
+    cab.set_sync_free(False)
+    y_c1 = cab(x, ids, w, sw)  # C ABI, v1
+    cab.set_sync_free(True)
     torch.cuda.synchronize()
-    assert torch.equal(y_py, y_c)
+    assert torch.equal(y_py, y_c) and torch.equal(y_v1, y_c) and torch.equal(y_c1, y_c)
     ref = oracle_run(oracle_layer(case), case)
     assert row_rel_err(y_c.float().cpu().numpy().astype(np.float64), ref) <= 1e-2
     assert cab.poll_error() == 0
