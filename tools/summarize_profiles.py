@@ -68,7 +68,16 @@ def main(src, dst):
             v = float(v.replace(",", ""))
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
+        # tagged with the library it was captured on (the capture must come from this tree's libmxmoe.so):
+        # bench.py reports roofline.traffic only for the same library build and token count
+        import hashlib
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from synth import configs as C
+        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2505_05799_b200",
+                               "libmxmoe.so"), "rb") as f:
+            sha = hashlib.sha1(f.read()).hexdigest()
         json.dump({"kernel": "moe_gemm_kernel", "config": f"{cfg} mixed (bench default tokens)",
+                   "tokens": C.get_config(cfg).tokens, "lib_sha1": sha,
                    "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                    "source": os.path.join(dst, f"ncu_{cfg}_summary.txt")},
                   open(os.path.join(os.path.dirname(dst.rstrip("/")), f"ncu_traffic_{cfg}.json"), "w"), indent=1)
