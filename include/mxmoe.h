@@ -216,11 +216,15 @@ int32_t mxm_kernels_per_call(const mxm_layer* l);
  *   XCA/XCB int32[G][R]         per-group sum of the a4 codes (offset-binary correction of w4a4 blocks)
  *   H bf16[R][F]  HQ int8[R][F]  HS f32[G][R]  HC int32[G][R]   the same for h (F = max inter, entry F_MAX)
  *   O bf16[R][hidden]           per-route down output o * w_e
- *   V_OFF int32[E+S+1] first row of each (virtual) expert;  R and F_MAX are values, not offsets. */
+ *   V_OFF int32[E+S+1] first row of each (virtual) expert;  R and F_MAX are values, not offsets.
+ *   TASKS 16-byte records {u16 expert, u8 phase, u8 nt, i32 row0, u16 rows, u16 ntile, i32 gid} in queue order
+ *   META int32: [0] tasks, [1..3] tasks per phase, [4] m-tile groups G, [5] queue head, [6] executed, [7] split-K
+ *                slices, then the group table grp_v / grp_row0 / grp_rows / grp_nt, G_MAX entries each;
+ *                G_MAX is a value. */
 enum {
   MXM_WS_ROW_SRC = 0, MXM_WS_ROW_W, MXM_WS_ROW_EXP, MXM_WS_INV, MXM_WS_XB, MXM_WS_XQA, MXM_WS_XSA, MXM_WS_XQB,
   MXM_WS_XSB, MXM_WS_H, MXM_WS_HQ, MXM_WS_HS, MXM_WS_O, MXM_WS_V_OFF, MXM_WS_R, MXM_WS_F_MAX, MXM_WS_XCA,
-  MXM_WS_XCB, MXM_WS_HC, MXM_WS_N
+  MXM_WS_XCB, MXM_WS_HC, MXM_WS_TASKS, MXM_WS_META, MXM_WS_G_MAX, MXM_WS_N
 };
 mxm_status mxm_debug_workspace_layout(const mxm_layer* l, int64_t T, int32_t top_k, int64_t* off);
 /* [sync] bytes of the accumulator dump buffer of mxm_debug_moe_group_gemm_dump for T tokens and top_k. */

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libmxmoe.so")
 MXM_OK, MXM_E_CONFIG, MXM_E_DATA, MXM_E_CUDA, MXM_E_NCCL = 0, 3, 4, 5, 6
 # include/mxmoe.h MXM_WS_* (workspace introspection, test-only)
 WS_NAMES = ["row_src", "row_w", "row_exp", "inv", "xb", "xqa", "xsa", "xqb", "xsb", "h", "hq", "hs", "o", "v_off",
-            "R", "f_max", "xca", "xcb", "hc"]
+            "R", "f_max", "xca", "xcb", "hc", "tasks", "meta", "g_max"]
 
 
 class MxmError(RuntimeError):

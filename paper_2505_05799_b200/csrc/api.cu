@@ -666,7 +666,8 @@ mxm_status mxm_debug_workspace_layout(const mxm_layer* l, int64_t T, int32_t k, 
   if (!l || !off || T < 0 || k <= 0 || k > 32) return fail(MXM_E_CONFIG, "bad argument");
   const WsLayout w = make_layout(l, T, k);
   const int64_t v[MXM_WS_N] = {w.row_src, w.row_w, w.row_exp, w.inv, w.Xb, w.XqA, w.XsA, w.XqB, w.XsB,
-                               w.H, w.Hq, w.Hs, w.O, w.v_off, w.R, l->f_max, w.XcA, w.XcB, w.Hc};
+                               w.H, w.Hq, w.Hs, w.O, w.v_off, w.R, l->f_max, w.XcA, w.XcB, w.Hc,
+                               w.tasks, w.meta, w.g_max};
   for (int i = 0; i < MXM_WS_N; ++i) off[i] = v[i];
   return MXM_OK;
 }
