@@ -103,6 +103,12 @@ struct mxm_layer {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::mutex side_mu;  // the fork / join events are per layer: concurrent calls serialise this section
+  // tensor maps of the token-tile operands of the last call (guarded by side_mu): re-encoded only when the
+  // workspace, T or top_k change (20 cuTensorMapEncodeTiled calls cost tens of us, a tenth of a T = 1 step)
+  const void* tm_ws = nullptr;
+  int64_t tm_T = -1;
+  int tm_k = 0;
+  CUtensorMap tm[5][4];
   ~mxm_layer() {
     for (auto e : prof_ev) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -515,12 +521,20 @@ static mxm_status run_group_gemm(const mxm_layer* l, const void* x, int64_t T, i
   const void* srcs[5] = {P(w.Xb), P(w.XqA), P(w.XqB), P(w.H), P(w.Hq)};
   const bool isbf[5] = {true, false, false, true, false};
   const uint64_t cols[5] = {(uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->f_max, (uint64_t)l->f_max};
-  for (int i = 0; i < 5; ++i) {
-    if (!srcs[i]) continue;
-    for (int j = 0; j < 4; ++j)
-      if (!encode_2d(&prm.tmap[i][j], srcs[i], isbf[i], cols[i], (uint64_t)w.R, boxes[j]))
-        return fail(MXM_E_CUDA, "cuTensorMapEncodeTiled failed");
+  if (ml->tm_ws != ws || ml->tm_T != T || ml->tm_k != k) {
+    ml->tm_ws = nullptr;
+    for (int i = 0; i < 5; ++i) {
+      if (!srcs[i]) continue;
+      for (int j = 0; j < 4; ++j)
+        if (!encode_2d(&ml->tm[i][j], srcs[i], isbf[i], cols[i], (uint64_t)w.R, boxes[j]))
+          return fail(MXM_E_CUDA, "cuTensorMapEncodeTiled failed");
+    }
+    ml->tm_ws = ws;
+    ml->tm_T = T;
+    ml->tm_k = k;
   }
+  for (int i = 0; i < 5; ++i)
+    if (srcs[i]) memcpy(&prm.tmap[i][0], &ml->tm[i][0], sizeof(ml->tm[i]));
   prm.ex = l->ex_dev;
   prm.tasks = (const Task*)P(w.tasks);
   prm.meta = (int32_t*)P(w.meta);

@@ -271,17 +271,19 @@ __device__ __forceinline__ void xform_wo(const uint8_t* __restrict__ raw, bool h
         o[8 * j + t] = deq_pair(and_or(word >> (2 * t), 0x00030003u, (((hw >> t) & 0x00010001u) << 2) | 0x43004300u),
                                 off2, s2, z2);
     }
-  } else {  // 8-bit: fp32 path (128 + u is not exact in bf16 for u >= 128)
-    const float sf = __uint_as_float(s2 << 16), zf = __uint_as_float(z2 << 16);
-    const float fo = (float)(off2 & 0xFFu);
+  } else {  // 8-bit: 128 + u is not exact in bf16 for u >= 128. q s + z is exact in fp64 (q s has 16 significant
+            // bits), so one rounding to bf16 gives R5's bf16_rne(q s + z); an fp32 sum would round twice
+    const double sd = (double)__uint_as_float(s2 << 16), zd = (double)__uint_as_float(z2 << 16);
+    const int fo = (int)(off2 & 0xFFu);
+    auto deq = [&](uint32_t u) { return __double2bfloat16(fma((double)((int)u - fo), sd, zd)); };
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t word = w[(8 * H + j) * 128 + r];
-      float f[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) f[b] = (__uint_as_float(0x4B000000u | ((word >> (8 * b)) & 0xFFu)) - 8388608.f) - fo;
-      __nv_bfloat162 lo = __floats2bfloat162_rn(fmaf(f[0], sf, zf), fmaf(f[1], sf, zf));
-      __nv_bfloat162 hi = __floats2bfloat162_rn(fmaf(f[2], sf, zf), fmaf(f[3], sf, zf));
+      __nv_bfloat162 lo, hi;
+      lo.x = deq(word & 0xFFu);
+      lo.y = deq((word >> 8) & 0xFFu);
+      hi.x = deq((word >> 16) & 0xFFu);
+      hi.y = deq(word >> 24);
       o[2 * j] = *reinterpret_cast<uint32_t*>(&lo);
       o[2 * j + 1] = *reinterpret_cast<uint32_t*>(&hi);
     }
