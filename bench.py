@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=128, help="tokens of the larger cpu_baseline oracle sample")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent full replicas instead of EP")
+    ap.add_argument("--placement", default="lpt", choices=["lpt", "contiguous"],
+                    help="N>1 expert parallelism: expert-to-rank placement (placement.py; LPT on the Zipf popularity)")
     return ap.parse_args()
 
 
@@ -345,8 +347,16 @@ def main():
     weights = gen_weights(cfg)
     Wt = [[to_bf16(b, dev) for b in blk] for blk in weights]
     use_ep = ws > 1 and not args.replicas
+    inv_place = None
     if use_ep:
         from paper_2505_05799_b200.ep import ExpertParallelMoE
+        from paper_2505_05799_b200.placement import apply_placement, inverse, lpt_placement
+        # expert placement: the experts are re-indexed offline (weights / table reordered; the router emits ids in
+        # the new order, here the synthetic ids are mapped through the inverse permutation)
+        perm = (lpt_placement(C.zipf_popularity(cfg.n_routed, 0.8, seed=0), ws) if args.placement == "lpt"
+                else np.arange(cfg.n_routed))
+        Wt, table = apply_placement(Wt, table, perm, cfg.n_routed)
+        inv_place = inverse(perm)
         ep = ExpertParallelMoE.from_weights(cfg.n_routed, cfg.n_shared, cfg.hidden, cfg.inter, cfg.shared_inter, Wt,
                                             table)
         layer = ep.local  # the rank's routed experts: the dominant kernel
@@ -357,6 +367,9 @@ def main():
     # per-rank batch: rank r uses seeds offset by r
     x_np = gen_activations(T, cfg.hidden, seed=1 + rank)
     ids_np, w_np = gen_routing(T, cfg.n_routed, cfg.top_k, seed=rank)
+    place = (lambda a: np.where(a >= 0, inv_place[np.maximum(a, 0)], -1).astype(np.int32)) if inv_place is not None \
+        else (lambda a: a)
+    ids_np = place(ids_np)
     sw_np = gen_shared_weights(T, cfg.n_shared, seed=2 + rank) if cfg.n_shared else None
     x = to_bf16(x_np, dev)
     ids = torch.from_numpy(ids_np).to(dev)
@@ -371,7 +384,7 @@ def main():
         wsb = None
         # the local layer's counts: every rank's routing restricted to this rank's experts (host, seeded)
         epr = cfg.n_routed // ws
-        all_ids = np.concatenate([gen_routing(T, cfg.n_routed, cfg.top_k, seed=r)[0] for r in range(ws)])
+        all_ids = place(np.concatenate([gen_routing(T, cfg.n_routed, cfg.top_k, seed=r)[0] for r in range(ws)]))
         loc = all_ids[(all_ids >= rank * epr) & (all_ids < (rank + 1) * epr)] - rank * epr
         counts_local = np.bincount(loc, minlength=epr)
     else:
@@ -517,7 +530,8 @@ def main():
                 "config": {"workload": cfg.name, "tokens_per_gpu": T, "experts": f"{cfg.n_routed}+{cfg.n_shared}",
                            "hidden": cfg.hidden, "inter": cfg.inter, "top_k": k, "table": args.table,
                            "l2": "flushed before every timed step (256 MB memset, untimed)",
-                           "parallelism": (f"ep{ws} (sync-free NCCL all-to-all dispatch/combine at fixed capacity, shared experts replicated)"
+                           "parallelism": (f"ep{ws} (sync-free NCCL all-to-all dispatch/combine at fixed capacity, "
+                                           f"{args.placement} expert placement, shared experts replicated)"
                                            if use_ep else f"replicas x{ws}") if ws > 1 else "single GPU"},
                 "roofline": roofline, "per_expert_roofline": per_expert, "stage_ms": stage_ms,
                 "cpu_baseline": cpu, "e2e": e2e, "comparators": comparators, "gpu_launches": launches * K, "clocks": clocks,
