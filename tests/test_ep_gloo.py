@@ -95,7 +95,19 @@ def _case():
     return cfg, table, make_case(cfg, table, 24, seed=3)
 
 
-def _worker(rank, world, port, out_path):
+def _placed_case(case, table, cfg, world):
+    """The same block with an LPT expert placement (placement.py): experts re-indexed, ids mapped."""
+    from paper_2505_05799_b200.placement import apply_placement, inverse, lpt_placement
+    ids = case["ids"]
+    loads = np.bincount(ids[ids >= 0], minlength=cfg.n_routed).astype(float)
+    perm = lpt_placement(loads, world)
+    w2, t2 = apply_placement(case["weights"], table, perm, cfg.n_routed)
+    inv = inverse(perm)
+    c2 = dict(case, weights=w2, ids=np.where(ids >= 0, inv[np.maximum(ids, 0)], -1).astype(np.int32))
+    return c2, t2
+
+
+def _worker(rank, world, port, out_path, placed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -103,6 +115,8 @@ def _worker(rank, world, port, out_path):
     from paper_2505_05799_b200.ep import ExpertParallelMoE
 
     cfg, table, case = _case()
+    if placed:
+        case, table = _placed_case(case, table, cfg, world)
     full = quantize_layer(case["weights"], table, cfg.n_routed, cfg.n_shared)
     epr = cfg.n_routed // world
     lo = rank * epr
@@ -141,6 +155,20 @@ def test_ep_two_ranks_equals_unsharded_oracle(tmp_path, world):
     # the sync-free exchange (fixed capacity, padding rows without routes) gives the same bits as v1
     y_sf = np.concatenate([np.load(f"{out}_sync_free_{r}.npy") for r in range(world)])
     assert np.array_equal(y, y_sf)
+    from oracle.moe import moe_block, quantize_layer
+    from tests.moe_cases import row_rel_err
+    cfg, table, case = _case()
+    ref = moe_block(case["x"], quantize_layer(case["weights"], table, cfg.n_routed, cfg.n_shared), case["ids"],
+                    case["w"], case["shared_w"])
+    assert row_rel_err(y.astype(np.float64), ref) <= 1e-2
+
+
+def test_ep_two_ranks_lpt_placement(tmp_path):
+    """LPT-placed experts over 2 gloo ranks (sync-free exchange) = the unsharded block with the original order."""
+    world = 2
+    out = str(tmp_path / "yp")
+    mp.spawn(_worker, args=(world, _free_port(), out, True), nprocs=world, join=True)
+    y = np.concatenate([np.load(f"{out}_sync_free_{r}.npy") for r in range(world)])
     from oracle.moe import moe_block, quantize_layer
     from tests.moe_cases import row_rel_err
     cfg, table, case = _case()
