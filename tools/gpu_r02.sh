@@ -17,14 +17,18 @@ if [ -n "$NCU" ]; then
      python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-comparators > /dev/null 2>$O/ncu1.err
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:moe_gemm -s 2 -c 1 -o $O/prof_q2 -f \
      python bench.py --steps 1 --warmup 2 --no-cpu-baseline --no-e2e --no-comparators > /dev/null 2>$O/ncu2.err
-  timeout 600 ncu --set full --clock-control none -k regex:gather_ -s 2 -c 1 -o $O/prof_q2_gather -f \
-     python bench.py --steps 1 --warmup 2 --no-cpu-baseline --no-e2e --no-comparators > /dev/null 2>$O/ncu3.err
   for c in ${NCU_CFGS:-}; do
     timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'route_|gather_|plan_|moe_gemm|combine_' -c 40 --csv --log-file $O/launches_$c.csv \
        python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-comparators > /dev/null 2>$O/ncu1_$c.err
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:moe_gemm -s 2 -c 1 -o $O/prof_$c -f \
        python bench.py --config $c --steps 1 --warmup 2 --no-cpu-baseline --no-e2e --no-comparators > /dev/null 2>$O/ncu2_$c.err
   done
+fi
+if [ -n "$NCU" ]; then
+  # summaries only travel back (gpurun_out is capped at 64 MiB): key counters + launch shares per config and the
+  # traffic json tagged with this library's sha, then the raw reports are dropped
+  python tools/summarize_profiles.py $O $O/summ > $O/summ.log 2>&1
+  rm -f $O/*.ncu-rep
 fi
 tail -2 $O/pytest_gpu.log; tail -1 $O/smoke.log
 for f in $O/bench_*.json; do echo $f; head -c 300 $f; echo; done
