@@ -1034,6 +1034,13 @@ namespace mxm { cudaError_t debug_nan_info(unsigned long long* out, bool reset);
 extern "C" int mxm_debug_nan_info(unsigned long long* out) { return (int)mxm::debug_nan_info(out, true); }
 #endif
 
+#ifdef MXM_TRACE_TASKS
+namespace mxm { cudaError_t debug_trace_tasks(unsigned long long* tt, unsigned long long* cta); }
+extern "C" int mxm_debug_trace_tasks(unsigned long long* tt, unsigned long long* cta) {
+  return (int)mxm::debug_trace_tasks(tt, cta);
+}
+#endif
+
 #ifdef MXM_TRACE
 namespace mxm { cudaError_t debug_trace(unsigned long long* out); }
 extern "C" int mxm_debug_trace(unsigned long long* out) { return (int)mxm::debug_trace(out); }

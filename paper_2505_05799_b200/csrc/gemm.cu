@@ -180,6 +180,17 @@ __device__ unsigned long long g_tr[13][kTrN];
 #else
 #define TR(ev, idx) do { } while (0)
 #endif
+#ifdef MXM_TRACE_TASKS
+// per-task timeline of CTA 0 and per-CTA start / end / counts (diagnostic build): tools/diag_tasks.py
+constexpr int kTtN = 4096, kTtCta = 160;
+__device__ unsigned long long g_tt[2][kTtN];   // [0] clock64 at task fetch, [1] phase | stages << 8 | nt << 32
+__device__ unsigned long long g_cta[kTtCta][4];  // globaltimer start, end, tasks, stages
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 // ---------------------------------------------------------------- transforms (one thread per A row)
 __device__ __forceinline__ uint32_t bf2_sub(uint32_t a, uint32_t b) {
   __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a), y = *reinterpret_cast<__nv_bfloat162*>(&b);
@@ -1180,6 +1191,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     uint32_t acc_ph = 0;  // bit b: parity of the next wait on acce[b] (phase bits, no local arrays)
     uint32_t aidx = 0;    // TS stages issued so far (A-ring slot and parity)
     int ntr_m = 0, nev_m = 0;
+#ifdef MXM_TRACE_TASKS
+    const unsigned long long tt_start = gtimer();
+    unsigned long long tt_tasks = 0, tt_stages = 0;
+#endif
     for (uint32_t it = 0;; ++it) {
       const uint32_t slot = it % kRing, rphase = (it / kRing) & 1;
       twait(&ctl.tfull[slot], rphase, pc[3], prof_on);
@@ -1187,11 +1202,32 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl.tempty[slot]);
       const uint32_t phase = bcast(t.phase);
+#ifdef MXM_TRACE_TASKS
+      if (phase == 255 && lane == 0 && blockIdx.x < kTtCta) {
+        g_cta[blockIdx.x][0] = tt_start;
+        g_cta[blockIdx.x][1] = gtimer();
+        g_cta[blockIdx.x][2] = tt_tasks;
+        g_cta[blockIdx.x][3] = tt_stages;
+      }
+#endif
       if (phase == 255) break;
       if (phase == 1) continue;
       SubLoop sl[2];
       const int nsl = (int)bcast((uint32_t)build_subloops(t, p.ex, p.d, n_split, sl));
       const uint32_t nt = bcast(t.nt);
+#ifdef MXM_TRACE_TASKS
+      {
+        unsigned long long nst = 0;
+        for (int si = 0; si < nsl; ++si) nst += (unsigned long long)(SPLIT ? sl[si].ks1 - sl[si].ks0 : sl[si].ns);
+        if (blockIdx.x == 0 && lane == 0 && tt_tasks < kTtN) {
+          g_tt[0][tt_tasks] = clock64();
+          g_tt[1][tt_tasks] = phase | (nst << 8) | ((unsigned long long)nt << 32) |
+                              ((unsigned long long)sl[0].g128 << 48);
+        }
+        ++tt_tasks;
+        tt_stages += nst;
+      }
+#endif
       for (int si = 0; si < nsl; ++si) {
         const SubLoop s = sl[si];
         const uint32_t ns = bcast((uint32_t)(SPLIT ? s.ks1 - s.ks0 : s.ns)), g128 = bcast((uint32_t)s.g128);
@@ -1832,6 +1868,12 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 
 #ifdef MXM_TRACE
 cudaError_t debug_trace(unsigned long long* out) { return cudaMemcpyFromSymbol(out, g_tr, sizeof(g_tr)); }
+#endif
+#ifdef MXM_TRACE_TASKS
+cudaError_t debug_trace_tasks(unsigned long long* tt, unsigned long long* cta) {
+  cudaError_t e = cudaMemcpyFromSymbol(tt, g_tt, sizeof(g_tt));
+  return e != cudaSuccess ? e : cudaMemcpyFromSymbol(cta, g_cta, sizeof(g_cta));
+}
 #endif
 #ifdef MXM_DEBUG_NAN
 cudaError_t debug_nan_info(unsigned long long* out, bool reset) {
