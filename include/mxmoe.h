@@ -214,7 +214,9 @@ int32_t mxm_kernels_per_call(const mxm_layer* l);
  *                               e4m3 byte (q<0)<<7 | |q|, whose value is q * 2^-9)
  *   XSA/XSB f32[G][R]           activation scales, group-major (G = hidden/128, or 1 per-token)
  *   XCA/XCB int32[G][R]         per-group sum of the a4 codes (offset-binary correction of w4a4 blocks)
- *   H bf16[R][F]  HQ int8[R][F]  HS f32[G][R]  HC int32[G][R]   the same for h (F = max inter, entry F_MAX)
+ *   H bf16, HQ int8: h rows in two regions, the T*n_shared shared rows [T*S][shared_inter] first, then the
+ *                               T*k routed rows [T*k][inter] (row r >= T*S at (T*S*shared_inter + (r-T*S)*inter))
+ *   HS f32[G][R]  HC int32[G][R]  scales / code sums of h (G = F/128, F = max inter, entry F_MAX)
  *   O bf16[R][hidden]           per-route down output o * w_e
  *   V_OFF int32[E+S+1] first row of each (virtual) expert;  R and F_MAX are values, not offsets.
  *   TASKS 16-byte records {u16 expert, u8 phase, u8 nt, i32 row0, u16 rows, u16 ntile, i32 gid} in queue order

@@ -108,7 +108,7 @@ struct mxm_layer {
   const void* tm_ws = nullptr;
   int64_t tm_T = -1;
   int tm_k = 0;
-  CUtensorMap tm[5][4];
+  CUtensorMap tm[7][4];
   ~mxm_layer() {
     for (auto e : prof_ev) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -153,8 +153,11 @@ static WsLayout make_layout(const mxm_layer* l, int64_t T, int k) {
   w.XsA = l->need_xqa ? take(4 * R * (l->d / 128)) : -1;
   w.XqB = l->need_xqb ? take(R * l->d) : -1;
   w.XsB = l->need_xqb ? take(4 * R * (l->d / 128)) : -1;
-  w.H = take(2 * R * l->f_max);
-  w.Hq = l->need_hq ? take(R * l->f_max) : -1;
+  // h rows in two regions (gemm.cu h_off): the T*S shared rows at the shared width, the T*k routed rows at the
+  // routed width (R x max width would hold 4.5x the bytes at Qwen2-57B: f_s 20480 vs f 2560)
+  const int64_t h_elems = T * l->S * l->fs + T * k * l->f;
+  w.H = take(2 * h_elems);
+  w.Hq = l->need_hq ? take(h_elems) : -1;
   w.Hs = l->need_hq ? take(4 * R * (l->f_max / 128)) : -1;
   w.hmax = l->need_hq ? take(4 * R) : -1;
   w.XcA = l->need_xqa ? take(4 * R * (l->d / 128)) : -1;
@@ -518,23 +521,35 @@ static mxm_status run_group_gemm(const mxm_layer* l, const void* x, int64_t T, i
   GemmParams prm;
   memset(&prm, 0, sizeof(prm));
   const uint32_t boxes[4] = {16, 32, 64, MXM_DUAL_TILE};
-  const void* srcs[5] = {P(w.Xb), P(w.XqA), P(w.XqB), P(w.H), P(w.Hq)};
-  const bool isbf[5] = {true, false, false, true, false};
-  const uint64_t cols[5] = {(uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->f_max, (uint64_t)l->f_max};
+  // H / Hq: routed region (maps 3, 4: rows T*k at width f, after the shared region) and shared region (maps 5,
+  // 6: rows T*S at width f_s), gemm.cu h_off
+  const int64_t srows = T * l->S, rrows = T * k, rbase = srows * l->fs;
+  const void* srcs[7] = {P(w.Xb), P(w.XqA), P(w.XqB), w.H >= 0 ? (void*)((char*)P(w.H) + 2 * rbase) : nullptr,
+                         w.Hq >= 0 ? (void*)((char*)P(w.Hq) + rbase) : nullptr, srows > 0 ? P(w.H) : nullptr,
+                         srows > 0 && w.Hq >= 0 ? P(w.Hq) : nullptr};
+  const bool isbf[7] = {true, false, false, true, false, true, false};
+  const uint64_t cols[7] = {(uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->d, (uint64_t)l->f, (uint64_t)l->f,
+                            (uint64_t)l->fs, (uint64_t)l->fs};
+  const uint64_t rows[7] = {(uint64_t)w.R, (uint64_t)w.R, (uint64_t)w.R, (uint64_t)rrows, (uint64_t)rrows,
+                            (uint64_t)srows, (uint64_t)srows};
   if (ml->tm_ws != ws || ml->tm_T != T || ml->tm_k != k) {
     ml->tm_ws = nullptr;
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < 7; ++i) {
       if (!srcs[i]) continue;
       for (int j = 0; j < 4; ++j)
-        if (!encode_2d(&ml->tm[i][j], srcs[i], isbf[i], cols[i], (uint64_t)w.R, boxes[j]))
+        if (!encode_2d(&ml->tm[i][j], srcs[i], isbf[i], cols[i], rows[i], boxes[j]))
           return fail(MXM_E_CUDA, "cuTensorMapEncodeTiled failed");
     }
     ml->tm_ws = ws;
     ml->tm_T = T;
     ml->tm_k = k;
   }
-  for (int i = 0; i < 5; ++i)
+  for (int i = 0; i < 7; ++i)
     if (srcs[i]) memcpy(&prm.tmap[i][0], &ml->tm[i][0], sizeof(ml->tm[i]));
+  prm.h_srows = srows;
+  prm.h_rbase = rbase;
+  prm.f_s = l->fs;
+  prm.f_r = l->f;
   prm.ex = l->ex_dev;
   prm.tasks = (const Task*)P(w.tasks);
   prm.meta = (int32_t*)P(w.meta);

@@ -690,11 +690,18 @@ __device__ __forceinline__ void drain_event_any(int half, float2 (&acc2)[32], ui
   }
 }
 
+// H / Hq row layout (api.cu make_layout): shared-expert rows [0, h_srows) at stride f_s, then the routed rows
+// at stride f_r, so the workspace holds sum over rows of that row's expert width instead of R x max(f, f_s)
+__device__ __forceinline__ int64_t h_off(const GemmParams& p, int64_t row) {
+  return row < p.h_srows ? row * p.f_s : p.h_rbase + (row - p.h_srows) * p.f_r;
+}
+__device__ __forceinline__ int64_t h_ld(const GemmParams& p, int64_t row) { return row < p.h_srows ? p.f_s : p.f_r; }
+
 // h for 8 token columns [colc, colc+8) of output channel n (= this thread's TMEM lane), already rounded to
 // bf16 (hb, DESIGN R16), in the form the down block consumes (dmode): 0 bf16 H; 1 bf16 H + row max|h| via
 // atomicMax (per-token W-A down, quantized later in one pass); 2 fused per-128-group quantization: the group
 // is exactly this tile's 128 channels, so codes + scale are produced here (DESIGN R9).
-// nv = valid columns from colc (rows of the m-tile), hrow = &H[row0 + colc][n] (row stride f_max).
+// nv = valid columns from colc (rows of the m-tile), hrow = &H[row0 + colc][n] (h_off / h_ld: the row's region).
 template <bool DUMP = false>
 __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int dmode, int qmax, int n, int colc, int nv,
                                      const uint16_t (&hb)[8], Ctl& ctl, int wg, int q, int lane, uint32_t& rbuf) {
@@ -702,10 +709,11 @@ __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int 
   if (dmode >= 2) {  // 2: int8 codes (w5a5 / w8a8 g128 down), 3: e4m3 codes + group code sums (w4a4 g128 down),
                      // 4: FP8 e4m3 codes (FP8 g128 down)
     if constexpr (DUMP) {  // test build: also keep the bf16 h the fused quantizer consumed (bit-exact h-quant test)
-      uint16_t* hrow = p.H + row0 * p.f_max + n;
+      uint16_t* hrow = p.H + h_off(p, row0) + n;
+      const int64_t ld = h_ld(p, row0);
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < nv) hrow[(int64_t)j * p.f_max] = hb[j];
+        if (j < nv) hrow[(int64_t)j * ld] = hb[j];
     }
     uint32_t m[8];
 #pragma unroll
@@ -727,18 +735,19 @@ __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int 
       }
       if (q == 0 && lane < nv) p.Hs[row0 + lane + (int64_t)t.ntile * p.hs_stride] = sc_l;
     }
-    int8_t* hq = p.Hq + row0 * p.f_max + n;
+    int8_t* hq = p.Hq + h_off(p, row0) + n;
+    const int64_t hld = h_ld(p, row0);
     int qi[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float r = __shfl_sync(0xffffffffu, r_l, j);
       if (dmode == 4) {
         qi[j] = 0;
-        if (j < nv) hq[(int64_t)j * p.f_max] = (int8_t)fp8_act_code(bf16f(hb[j]), r);
+        if (j < nv) hq[(int64_t)j * hld] = (int8_t)fp8_act_code(bf16f(hb[j]), r);
         continue;
       }
       qi[j] = (int)fminf(fmaxf(rintf(__fmul_rn(bf16f(hb[j]), r)), -fq), fq);
-      if (j < nv) hq[(int64_t)j * p.f_max] = (int8_t)(dmode == 3 ? code_byte<true>(qi[j]) : code_byte<false>(qi[j]));
+      if (j < nv) hq[(int64_t)j * hld] = (int8_t)(dmode == 3 ? code_byte<true>(qi[j]) : code_byte<false>(qi[j]));
     }
     if (dmode == 3) {  // sum of the group's codes per token column: warp sums, then the 4 warps of the warpgroup
       int cs[8];
@@ -757,10 +766,11 @@ __device__ __forceinline__ void emit_h8(const GemmParams& p, const Task& t, int 
     rbuf ^= 1;
     return;
   }
-  uint16_t* hrow = p.H + row0 * p.f_max + n;
+  uint16_t* hrow = p.H + h_off(p, row0) + n;
+  const int64_t ld = h_ld(p, row0);
 #pragma unroll
   for (int j = 0; j < 8; ++j)
-    if (j < nv) hrow[(int64_t)j * p.f_max] = hb[j];
+    if (j < nv) hrow[(int64_t)j * ld] = hb[j];
   if (dmode == 1) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -967,7 +977,16 @@ __device__ __forceinline__ void copy_task(const GemmParams& p, const Task& t, Ct
   const int nti = nt_index(t.nt);
   for (int si = 0; si < nsl; ++si) {
     const SubLoop s = sl[si];
-    const CUtensorMap* map = &p.tmap[s.bmap][nti];
+    // h inputs of a down (maps 3, 4): shared rows use the shared-region maps (5, 6), routed rows their own
+    // region's maps with region-relative row coordinates
+    int bm = s.bmap, trow = t.row0;
+    if (bm >= 3) {
+      if (t.row0 < p.h_srows)
+        bm += 2;
+      else
+        trow = (int)(t.row0 - p.h_srows);
+    }
+    const CUtensorMap* map = &p.tmap[bm][nti];
     // per-mat chunk streams (gate and up may differ in bits / group / format)
     const PackGeom& g0 = s.mat[0]->geo;
     const PackGeom& g1 = s.mat[s.nmats - 1]->geo;
@@ -1015,7 +1034,7 @@ __device__ __forceinline__ void copy_task(const GemmParams& p, const Task& t, Ct
         if (e1) bulk_load(slot + 2 * kTileBytes, gm1, e1, &ctl.full[stage]);
         bulk_load(slot + 2 * kTileBytes + e1, src1, c1, &ctl.full[stage]);
       }
-      if (ROLE == 1) tma_load_2d(slot, map, &ctl.full[stage], ks * kstep, t.row0);
+      if (ROLE == 1) tma_load_2d(slot, map, &ctl.full[stage], ks * kstep, trow);
       src0 += c0;
       gm0 = nullptr;
       if (src1) {
@@ -1127,7 +1146,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
   }
   if (warp == 1) tmem_alloc<512>(&ctl.tmem_base);
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 5; ++i)
+    for (int i = 0; i < 7; ++i)
       for (int j = 0; j < 4; ++j) prefetch_tmap(&p.tmap[i][j]);
   }
   tc_fence_before();
@@ -1422,8 +1441,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
           const float amax = __uint_as_float(__ldcg(p.hmax + row));
           const float r = amax > 0.f ? __fdiv_rn(fq, amax) : 0.f;
           const float sc = amax > 0.f ? __fdiv_rn(amax, fq) : 1.f;
-          const uint4* src = reinterpret_cast<const uint4*>(p.H + row * p.f_max);
-          uint2* dst = reinterpret_cast<uint2*>(p.Hq + row * p.f_max);
+          const uint4* src = reinterpret_cast<const uint4*>(p.H + h_off(p, row));
+          uint2* dst = reinterpret_cast<uint2*>(p.Hq + h_off(p, row));
           // kU 16-byte loads in flight per lane before any store (a single load per iteration leaves this pass
           // latency-bound at a few GB/s per SM)
           constexpr int kU = 8;

@@ -9,7 +9,8 @@
 namespace mxm {
 
 struct GemmParams {
-  CUtensorMap tmap[5][4];  // B sources {Xb, XqA, XqB, H, Hq} x token tile {16, 32, 64, 96}
+  // B sources {Xb, XqA, XqB, H routed, Hq routed, H shared, Hq shared} x token tile {16, 32, 64, 96}
+  CUtensorMap tmap[7][4];
   const ExpertDesc* ex;
   const Task* tasks;
   int32_t* meta;  // [0] n_tasks, [5] queue head, [6] executed tasks
@@ -30,6 +31,10 @@ struct GemmParams {
   float* P;          // split-K fp32 partials [kSplitMax][kSplitRows][d] (nullptr: no split-K this launch)
   int32_t* red_cnt;  // split-K arrival counters [group][d/128]
   int d, f_max;
+  // H / Hq rows in two regions: shared rows [0, h_srows) at row stride f_s, then routed rows at stride f_r
+  // (element offset of the routed region h_rbase = h_srows * f_s); gemm.cu h_off
+  int64_t h_srows, h_rbase;
+  int f_s, f_r;
   unsigned long long* prof;  // optional [grid][16] cycle counters per wait site (nullptr = off)
   // test-only accumulator dump (mxm_debug_moe_group_gemm_dump; nullptr in the product launch): the raw 32-bit
   // accumulator of every weight-activation drain event (layout: gemm.cu dump_index)

@@ -83,6 +83,17 @@ def _acc_as_int(raw_u32: np.ndarray, f8: bool, qsum: np.ndarray) -> np.ndarray:
     return v.astype(np.int64) - 8 * qsum[:, None]
 
 
+def _h_rows(ws, off, dtype, case, rows, v):
+    """h / h-code rows of expert v from the two-region layout (include/mxmoe.h MXM_WS_H): the T*S shared rows at
+    the shared width first, then the routed rows at the routed width."""
+    cfg, T, k = case["cfg"], case["T"], case["k"]
+    srows, fs, f = T * cfg.n_shared, cfg.shared_inter if cfg.n_shared else 0, cfg.inter
+    if v >= cfg.n_routed:
+        return _view(ws, off, dtype, srows * fs).reshape(srows, fs)[rows]
+    base = off + srows * fs * np.dtype(dtype).itemsize
+    return _view(ws, base, dtype, T * k * f).reshape(T * k, f)[rows - srows]
+
+
 def check_case(mx, case, min_rows=1):
     cfg, table = case["cfg"], case["table"]
     E, S, d = cfg.n_routed, cfg.n_shared, cfg.hidden
@@ -131,10 +142,10 @@ def check_case(mx, case, min_rows=1):
         sch = table[v][2]
         if sch.a_bits != 16:
             G = f // 128 if sch.a_group == 128 else 1
-            h_bits = _view(ws, lay["h"], np.uint16, R * F).reshape(R, F)[rows][:, :f]
+            h_bits = _h_rows(ws, lay["h"], np.uint16, case, rows, v)
             hin = bf16_bits_to_f64(h_bits).astype(np.float32)
             q_ref, s_ref, qs_ref = quantize_act(hin, sch.a_bits, sch.a_group)
-            codes = decode_codes(_view(ws, lay["hq"], np.uint8, R * F).reshape(R, F)[rows][:, :f], sch.a_bits)
+            codes = decode_codes(_h_rows(ws, lay["hq"], np.uint8, case, rows, v), sch.a_bits)
             scales = _view(ws, lay["hs"], np.float32, (F // 128) * R).reshape(F // 128, R)[:G, rows].T
             assert np.array_equal(codes, q_ref), f"expert {v} down: h codes"
             assert np.array_equal(scales, s_ref), f"expert {v} down: h scales"
