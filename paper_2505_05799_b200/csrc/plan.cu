@@ -18,7 +18,24 @@ constexpr int kPlanThreads = 1024;
 #ifndef MXM_NMAJOR_MIN_GROUPS
 #define MXM_NMAJOR_MIN_GROUPS 2  // experts with at least this many full m-tiles are emitted n-tile-major (0 = off)
 #endif
+#ifndef MXM_BAND_MB
+#define MXM_BAND_MB 32  // n-tile-major emission in bands of m-tiles whose input rows total <= this many MiB (0: one band)
+#endif
 constexpr int kMaxV = 256;
+
+// m-tiles per band of an n-tile-major expert: its input rows (row_bytes each, nt rows per m-tile) stay in L2 while
+// every n-tile of the band runs; at least 2 m-tiles, at most the expert's nf full m-tiles
+__device__ __forceinline__ int band_groups(int64_t row_bytes, int nt, int nf) {
+  if (MXM_BAND_MB <= 0) return nf;
+  const int64_t b = ((int64_t)MXM_BAND_MB << 20) / (row_bytes * nt > 0 ? row_bytes * nt : 1);
+  return (int)(b < 2 ? 2 : (b > nf ? nf : b));
+}
+// queue slot of (m-tile i, n-task j) inside an expert's block of nf x n tasks: bands of B m-tiles, n-tile-major
+// within a band
+__device__ __forceinline__ int64_t band_pos(int i, int j, int nf, int n, int B) {
+  const int b = i / B, ii = i - b * B, Bb = min(B, nf - b * B);
+  return (int64_t)b * B * n + (int64_t)j * Bb + ii;
+}
 
 // exclusive block-wide scan of one int per thread (kPlanThreads threads); returns the block total
 __device__ int block_excl_scan(int v, int* warp_tot, int* out_total) {
@@ -251,13 +268,21 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
     // within its (contiguous) block of full groups: CTAs running side by side then share one weight tile
     // in L2 and stream different token tiles, instead of sharing a token tile and each streaming its own
     // weight tile (a large expert's weights do not fit in L2 and were re-read from HBM per m-tile)
+    // A shared expert over all T tokens has more input rows than L2 holds next to the other experts' traffic
+    // (Qwen2-57B: 16384 x 3584 codes for gate/up, 16384 x 20480 h codes for the down), so its m-tiles are
+    // banded: n-tile-major within bands of m-tiles whose rows fit in MXM_BAND_MB (band_groups)
     const int nf = s_nfull[v], i = g - s_base[v];
     const bool nmajor = MXM_NMAJOR_MIN_GROUPS > 0 && nf >= MXM_NMAJOR_MIN_GROUPS && i >= 0 && i < nf;
     const int n1 = grp_n1[g], n2 = grp_n2[g];
+    const ExpertDesc& ev = ex[v];
+    const int64_t rb1 = (int64_t)d * (ev.blk[0].in_slot == 0 ? 2 : 1) +
+                        (ev.blk[1].in_slot != ev.blk[0].in_slot ? (int64_t)d * (ev.blk[1].in_slot == 0 ? 2 : 1) : 0);
+    const int64_t rb2 = (int64_t)ev.inter * (ev.blk[2].in_slot == 0 ? 2 : 1);
+    const int B1 = band_groups(rb1, t.nt, nf), B2 = band_groups(rb2, t.nt, nf);
     t.phase = 0;
     for (int j = 0; j < n1; ++j) {
       t.ntile = (uint16_t)j;
-      tasks[nmajor ? o1 - (int64_t)i * n1 + (int64_t)j * nf + i : o1 + j] = t;
+      tasks[nmajor ? o1 - (int64_t)i * n1 + band_pos(i, j, nf, n1, B1) : o1 + j] = t;
     }
     o1 += n1;
     t.phase = 1;
@@ -269,7 +294,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
     const int S_g = (S > 1 && down_splittable(ex[v])) ? S : 1;
     for (int j = 0; j < n2; ++j) {
       t.ntile = (uint16_t)((j / S_g) | ((j % S_g) << 10));  // down tile (or pair) index | K-slice << 10
-      tasks[nmajor ? o2 - (int64_t)i * n2 + (int64_t)j * nf + i : o2 + j] = t;
+      tasks[nmajor ? o2 - (int64_t)i * n2 + band_pos(i, j, nf, n2, B2) : o2 + j] = t;
     }
     o2 += n2;
   }
