@@ -221,7 +221,13 @@ __global__ void gather_quant_kernel(const uint16_t* __restrict__ x, int d, const
 // that format (k routed rows via inv[], S shared rows s*T + t). Same arithmetic as quant_row_warp (DESIGN R9):
 // every stored row is bit-identical to the row-major kernel's. Format a_bits 16 = the bf16 row copy (Xb).
 template <int MAXG>
-__global__ void __launch_bounds__(256) gather_tok_kernel(
+#ifndef MXM_GATHER_MINB
+#define MXM_GATHER_MINB 4  // resident 256-thread blocks per SM the register budget is sized for
+#endif
+#ifndef MXM_GATHER_PASS
+#define MXM_GATHER_PASS 8  // 128-element chunks per register pass (8, 16 measured: profiles/r02/ab_experiments.txt ab18)
+#endif
+__global__ void __launch_bounds__(256, MXM_GATHER_MINB) gather_tok_kernel(
     const uint16_t* __restrict__ x, int d, int64_t T, int k, int S, int E, const int32_t* __restrict__ inv,
     const int32_t* __restrict__ row_exp, const ExpertDesc* __restrict__ ex, ActFormats fm, int64_t R,
     uint16_t* __restrict__ Xb, int8_t* __restrict__ XqA, float* __restrict__ XsA, int8_t* __restrict__ XqB,
@@ -254,19 +260,29 @@ __global__ void __launch_bounds__(256) gather_tok_kernel(
   if (todo == 0) return;
   const int nch = d / 128;
   const uint16_t* src = x + t * d;
-  uint2 v[MAXG];
-#pragma unroll
-  for (int i = 0; i < MAXG; ++i)
-    if (i < nch) v[i] = *reinterpret_cast<const uint2*>(src + 128 * i + 4 * lane);
+  // the row in passes of kPass 128-element chunks: the register tile (3 x kPass words) fits 64 registers, so 4
+  // blocks stay resident per SM instead of 2 -- the kernel is latency-bound (ncu: 25 % occupancy, issue 28 %)
+  constexpr int kPass = MAXG < MXM_GATHER_PASS ? MAXG : MXM_GATHER_PASS;
+  auto load_chunk = [&](int i) { return *reinterpret_cast<const uint2*>(src + 128 * i + 4 * lane); };
   if (fb == 16) {  // bf16 copy into every weight-only / 16-bit route row of the token
+    for (int c0 = 0; c0 < nch; c0 += kPass) {
+      uint2 v[kPass];
+#pragma unroll
+      for (int i = 0; i < kPass; ++i)
+        if (c0 + i < nch) v[i] = load_chunk(c0 + i);
+      for (unsigned m = todo; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const int64_t r = __shfl_sync(0xffffffffu, row, j);
+        uint16_t* dst = Xb + r * d;
+#pragma unroll
+        for (int i = 0; i < kPass; ++i)
+          if (c0 + i < nch) *reinterpret_cast<uint2*>(dst + 128 * (c0 + i) + 4 * lane) = v[i];
+      }
+    }
     for (unsigned m = todo; m; m &= m - 1) {
       const int j = __ffs(m) - 1;
       const int64_t r = __shfl_sync(0xffffffffu, row, j);
       const int g0 = __shfl_sync(0xffffffffu, sl0, j);
-      uint16_t* dst = Xb + r * d;
-#pragma unroll
-      for (int i = 0; i < MAXG; ++i)
-        if (i < nch) *reinterpret_cast<uint2*>(dst + 128 * i + 4 * lane) = v[i];
       if (lane == 0 && g0 >= 0 && hmax) hmax[r] = 0u;
     }
     return;
@@ -294,46 +310,72 @@ __global__ void __launch_bounds__(256) gather_tok_kernel(
     }
     return packed;
   };
-  uint32_t code[MAXG];
-  float my_s = 1.f;  // g128: lane i holds group i's scale and code sum; per token: lane 0 the row's
+  float my_s = 1.f;  // g128: lane i holds group i's scale and code sum; per token: the row's
   int my_qs = 0;
-  if (fg == 128) {
+  // per token: the row maximum first (a load-only pass; the quantizing pass re-reads the row from L1)
+  float r_row = 0.f;
+  int qsum_row = 0;
+  if (fg != 128) {
+    float amax = 0.f;
+    for (int i = 0; i < nch; ++i) amax = fmaxf(amax, absmax4(load_chunk(i)));
+    amax = warp_max(amax);
+    if (amax > 0.f) {
+      r_row = __fdiv_rn(fq, amax);
+      my_s = __fdiv_rn(amax, fq);
+    }
+  }
+  for (int c0 = 0; c0 < nch; c0 += kPass) {
+    uint2 v[kPass];
 #pragma unroll
-    for (int i = 0; i < MAXG; ++i) {
-      if (i < nch) {
-        const float amax = warp_max(absmax4(v[i]));
-        float r = 0.f, s = 1.f;
-        if (amax > 0.f) {
-          r = __fdiv_rn(fq, amax);
-          s = __fdiv_rn(amax, fq);
-        }
-        int qsum = 0;
-        code[i] = quant4(v[i], r, qsum);
-        qsum = warp_sum(qsum);
-        if (lane == i) {
-          my_s = s;
-          my_qs = qsum;
+    for (int i = 0; i < kPass; ++i)
+      if (c0 + i < nch) v[i] = load_chunk(c0 + i);
+    uint32_t code[kPass];
+    if (fg == 128) {
+      // the pass's group maxima (independent reductions), then lane c divides for group c only (two IEEE
+      // divisions per lane instead of a dependent chain of 2 per group), r broadcast per group
+      float my_amax = 0.f;
+#pragma unroll
+      for (int i = 0; i < kPass; ++i) {
+        if (c0 + i < nch) {
+          const float amax = warp_max(absmax4(v[i]));
+          if (lane == c0 + i) my_amax = amax;
         }
       }
-    }
-  } else {
-    float amax = 0.f;
+      float r_l = 0.f;
+      if (my_amax > 0.f) {
+        r_l = __fdiv_rn(fq, my_amax);
+        my_s = __fdiv_rn(my_amax, fq);
+      }
 #pragma unroll
-    for (int i = 0; i < MAXG; ++i)
-      if (i < nch) amax = fmaxf(amax, absmax4(v[i]));
-    amax = warp_max(amax);
-    float r = 0.f, s = 1.f;
-    if (amax > 0.f) {
-      r = __fdiv_rn(fq, amax);
-      s = __fdiv_rn(amax, fq);
-    }
-    int qsum = 0;
+      for (int i = 0; i < kPass; ++i) {
+        if (c0 + i < nch) {
+          const float r = __shfl_sync(0xffffffffu, r_l, c0 + i);
+          int qsum = 0;
+          code[i] = quant4(v[i], r, qsum);
+          qsum = warp_sum(qsum);
+          if (lane == c0 + i) my_qs = qsum;
+        }
+      }
+    } else {
 #pragma unroll
-    for (int i = 0; i < MAXG; ++i)
-      if (i < nch) code[i] = quant4(v[i], r, qsum);
-    my_s = s;
-    my_qs = warp_sum(qsum);
+      for (int i = 0; i < kPass; ++i)
+        if (c0 + i < nch) code[i] = quant4(v[i], r_row, qsum_row);
+    }
+    for (unsigned m = todo; m; m &= m - 1) {
+      const int j = __ffs(m) - 1;
+      const int64_t r = __shfl_sync(0xffffffffu, row, j);
+      const int g0 = __shfl_sync(0xffffffffu, sl0, j), g1 = __shfl_sync(0xffffffffu, sl1, j);
+      for (int b = 0; b < 2; ++b) {
+        const int slot = b == 0 ? g0 : g1;
+        if (slot < 1) continue;
+        int8_t* q = (slot == 1 ? XqA : XqB) + r * d;
+#pragma unroll
+        for (int i = 0; i < kPass; ++i)
+          if (c0 + i < nch) *reinterpret_cast<uint32_t*>(q + 128 * (c0 + i) + 4 * lane) = code[i];
+      }
+    }
   }
+  if (fg != 128) my_qs = warp_sum(qsum_row);
   const int ng = fg == 128 ? nch : 1;
   for (unsigned m = todo; m; m &= m - 1) {
     const int j = __ffs(m) - 1;
@@ -342,12 +384,8 @@ __global__ void __launch_bounds__(256) gather_tok_kernel(
     for (int b = 0; b < 2; ++b) {
       const int slot = b == 0 ? g0 : g1;
       if (slot < 1) continue;
-      int8_t* q = (slot == 1 ? XqA : XqB) + r * d;
       float* sc = (slot == 1 ? XsA : XsB) + r;  // group-major [g][R]
       int32_t* qs = (slot == 1 ? XcA : XcB) + r;
-#pragma unroll
-      for (int i = 0; i < MAXG; ++i)
-        if (i < nch) *reinterpret_cast<uint32_t*>(q + 128 * i + 4 * lane) = code[i];
       if (lane < ng) {
         sc[(int64_t)lane * R] = my_s;
         qs[(int64_t)lane * R] = my_qs;
