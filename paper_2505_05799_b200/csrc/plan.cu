@@ -23,6 +23,14 @@ constexpr int kPlanThreads = 1024;
 #endif
 constexpr int kMaxV = 256;
 
+// one 16-byte store per task: the plan is a single block whose scattered task stores bound it (4-byte field
+// stores issued 4 L2 transactions per lane and task: Q2 plan 239 us, ncu profiles/r02/ncu_plan_q2.txt)
+__device__ __forceinline__ void st_task(Task* dst, const Task& t) {
+  uint4 u;
+  memcpy(&u, &t, sizeof(u));
+  *reinterpret_cast<uint4*>(dst) = u;
+}
+
 // m-tiles per band of an n-tile-major expert: its input rows (row_bytes each, nt rows per m-tile) stay in L2 while
 // every n-tile of the band runs; at least 2 m-tiles, at most the expert's nf full m-tiles
 __device__ __forceinline__ int band_groups(int64_t row_bytes, int nt, int nf) {
@@ -203,9 +211,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
   }
   __shared__ int s_wt[32];
   int t1, tq, t2;
-  const int e1 = block_excl_scan(c1, s_wt, &t1);
-  const int eq = block_excl_scan(cq, s_wt, &tq);
-  int e2 = block_excl_scan(c2, s_wt, &t2);
+  // phase totals (the per-group offsets are scanned again per emission round below)
+  block_excl_scan(c1, s_wt, &t1);
+  block_excl_scan(cq, s_wt, &tq);
+  block_excl_scan(c2, s_wt, &t2);
   // split-K of the downs when they cannot fill the SMs (common.cuh); red_cnt == nullptr: not allowed.
   // One slice count S for every splittable down of the launch (the last-arriver reduce counts S arrivals), so
   // S must give every splittable expert a non-empty last slice (experts may differ in ns: shared_inter != inter)
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
       if (down_splittable(ex[grp_v[g]])) grp_n2[g] *= S;
       c2 += grp_n2[g];
     }
-    e2 = block_excl_scan(c2, s_wt, &t2);
+    block_excl_scan(c2, s_wt, &t2);
     for (int i = tid; i < G * nd; i += kPlanThreads) red_cnt[i] = 0;
   }
   const int64_t total = (int64_t)t1 + tq + t2;
@@ -255,48 +264,63 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const ExpertDesc* __
     meta[7] = S;  // split-K slices of splittable down tasks
   }
   if (total > task_cap) return;
-  int64_t o1 = e1, oq = (int64_t)t1 + eq, o2 = (int64_t)t1 + tq + e2;
-  for (int g = g0; g < g1; ++g) {
-    Task t;
-    const int v = grp_v[g];
-    t.expert = (uint16_t)v;
-    t.row0 = grp_row0[g];
-    t.rows = (uint16_t)grp_rows[g];
-    t.nt = (uint8_t)grp_nt[g];
-    t.gid = g;
-    // an expert with many full m-tiles (e.g. a shared expert over all T tokens) is emitted n-tile-major
-    // within its (contiguous) block of full groups: CTAs running side by side then share one weight tile
-    // in L2 and stream different token tiles, instead of sharing a token tile and each streaming its own
-    // weight tile (a large expert's weights do not fit in L2 and were re-read from HBM per m-tile)
-    // A shared expert over all T tokens has more input rows than L2 holds next to the other experts' traffic
-    // (Qwen2-57B: 16384 x 3584 codes for gate/up, 16384 x 20480 h codes for the down), so its m-tiles are
-    // banded: n-tile-major within bands of m-tiles whose rows fit in MXM_BAND_MB (band_groups)
-    const int nf = s_nfull[v], i = g - s_base[v];
-    const bool nmajor = MXM_NMAJOR_MIN_GROUPS > 0 && nf >= MXM_NMAJOR_MIN_GROUPS && i >= 0 && i < nf;
-    const int n1 = grp_n1[g], n2 = grp_n2[g];
-    const ExpertDesc& ev = ex[v];
-    const int64_t rb1 = (int64_t)d * (ev.blk[0].in_slot == 0 ? 2 : 1) +
-                        (ev.blk[1].in_slot != ev.blk[0].in_slot ? (int64_t)d * (ev.blk[1].in_slot == 0 ? 2 : 1) : 0);
-    const int64_t rb2 = (int64_t)ev.inter * (ev.blk[2].in_slot == 0 ? 2 : 1);
-    const int B1 = band_groups(rb1, t.nt, nf), B2 = band_groups(rb2, t.nt, nf);
-    t.phase = 0;
-    for (int j = 0; j < n1; ++j) {
-      t.ntile = (uint16_t)j;
-      tasks[nmajor ? o1 - (int64_t)i * n1 + band_pos(i, j, nf, n1, B1) : o1 + j] = t;
+  // emission in rounds of kPlanThreads consecutive groups, one per thread (per-round scans give each group's
+  // offsets; the queue is the same as a per-thread contiguous range would write): consecutive lanes own
+  // consecutive m-tiles, so the n-tile-major blocks of large experts are written as contiguous 512-B runs
+  int64_t b1 = 0, bq = 0, b2 = 0;  // tasks of the groups of earlier rounds, per phase
+  for (int r0 = 0; r0 < G; r0 += kPlanThreads) {
+    const int g = r0 + tid;
+    const bool own = g < G;
+    int rt1, rtq, rt2;
+    const int x1 = block_excl_scan(own ? grp_n1[g] : 0, s_wt, &rt1);
+    const int xq = block_excl_scan(own ? grp_nq[g] : 0, s_wt, &rtq);
+    const int x2 = block_excl_scan(own ? grp_n2[g] : 0, s_wt, &rt2);
+    if (own) {
+      int64_t o1 = b1 + x1, oq = (int64_t)t1 + bq + xq, o2 = (int64_t)t1 + tq + b2 + x2;
+      Task t;
+      const int v = grp_v[g];
+      t.expert = (uint16_t)v;
+      t.row0 = grp_row0[g];
+      t.rows = (uint16_t)grp_rows[g];
+      t.nt = (uint8_t)grp_nt[g];
+      t.gid = g;
+      // an expert with many full m-tiles (e.g. a shared expert over all T tokens) is emitted n-tile-major
+      // within its (contiguous) block of full groups: CTAs running side by side then share one weight tile
+      // in L2 and stream different token tiles, instead of sharing a token tile and each streaming its own
+      // weight tile (a large expert's weights do not fit in L2 and were re-read from HBM per m-tile)
+      // A shared expert over all T tokens has more input rows than L2 holds next to the other experts' traffic
+      // (Qwen2-57B: 16384 x 3584 codes for gate/up, 16384 x 20480 h codes for the down), so its m-tiles are
+      // banded: n-tile-major within bands of m-tiles whose rows fit in MXM_BAND_MB (band_groups)
+      const int nf = s_nfull[v], i = g - s_base[v];
+      const bool nmajor = MXM_NMAJOR_MIN_GROUPS > 0 && nf >= MXM_NMAJOR_MIN_GROUPS && i >= 0 && i < nf;
+      const int n1 = grp_n1[g], n2 = grp_n2[g];
+      const ExpertDesc& ev = ex[v];
+      const int64_t rb1 = (int64_t)d * (ev.blk[0].in_slot == 0 ? 2 : 1) +
+                          (ev.blk[1].in_slot != ev.blk[0].in_slot ? (int64_t)d * (ev.blk[1].in_slot == 0 ? 2 : 1) : 0);
+      const int64_t rb2 = (int64_t)ev.inter * (ev.blk[2].in_slot == 0 ? 2 : 1);
+      const int B1 = band_groups(rb1, t.nt, nf), B2 = band_groups(rb2, t.nt, nf);
+      t.phase = 0;
+      for (int j = 0; j < n1; ++j) {
+        t.ntile = (uint16_t)j;
+        st_task(&tasks[nmajor ? o1 - (int64_t)i * n1 + band_pos(i, j, nf, n1, B1) : o1 + j], t);
+      }
+      o1 += n1;
+      t.phase = 1;
+      for (int j = 0; j < grp_nq[g]; ++j) {
+        t.ntile = (uint16_t)j;  // 32-row sub-chunk index
+        st_task(&tasks[oq++], t);
+      }
+      t.phase = 2;
+      const int S_g = (S > 1 && down_splittable(ex[v])) ? S : 1;
+      for (int j = 0; j < n2; ++j) {
+        t.ntile = (uint16_t)((j / S_g) | ((j % S_g) << 10));  // down tile (or pair) index | K-slice << 10
+        st_task(&tasks[nmajor ? o2 - (int64_t)i * n2 + band_pos(i, j, nf, n2, B2) : o2 + j], t);
+      }
+      o2 += n2;
     }
-    o1 += n1;
-    t.phase = 1;
-    for (int j = 0; j < grp_nq[g]; ++j) {
-      t.ntile = (uint16_t)j;  // 32-row sub-chunk index
-      tasks[oq++] = t;
-    }
-    t.phase = 2;
-    const int S_g = (S > 1 && down_splittable(ex[v])) ? S : 1;
-    for (int j = 0; j < n2; ++j) {
-      t.ntile = (uint16_t)((j / S_g) | ((j % S_g) << 10));  // down tile (or pair) index | K-slice << 10
-      tasks[nmajor ? o2 - (int64_t)i * n2 + band_pos(i, j, nf, n2, B2) : o2 + j] = t;
-    }
-    o2 += n2;
+    b1 += rt1;
+    bq += rtq;
+    b2 += rt2;
   }
   __syncthreads();  // every thread has read its grp_n2 entries before the scratch is cleared
   for (int g = tid; g < G; g += kPlanThreads) hq_done[g] = 0;
