@@ -65,16 +65,91 @@ __global__ void __launch_bounds__(256) gemv_w4(const uint32_t* __restrict__ q, c
   }
 }
 
+
+// v2: 16-B weight loads (lane = 32 consecutive k of one 1024-k chunk, one group scale per chunk), two rows per
+// warp in flight, nibble pairs dequantized as bf16x2 with the 0x4300 magic (w = (128 + q) s + (z - 128 s)),
+// fp32 accumulation
 template <int M>
+__global__ void __launch_bounds__(256) gemv_w4_v2(const uint32_t* __restrict__ q, const __nv_bfloat162* __restrict__ sz,
+                                                  const __nv_bfloat16* __restrict__ x, float* __restrict__ y, int N,
+                                                  int K) {
+  extern __shared__ __align__(16) __nv_bfloat16 xs[];  // [M][K]
+  for (int i = threadIdx.x * 8; i < M * K; i += blockDim.x * 8)
+    *reinterpret_cast<uint4*>(xs + i) = *reinterpret_cast<const uint4*>(x + i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nch = K / 1024, ng = K / 128;
+  constexpr int R = 2;
+  for (int n0 = (blockIdx.x * 8 + wib) * R; n0 < N; n0 += gridDim.x * 8 * R) {
+    uint4 wv[R][4];
+    float2 szf[R][4];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < nch && n0 + r < N) {
+          // chunk c of row n0 + r: k = 1024 c + 32 lane .. +32 = words 128 c + 4 lane .. +4 (the probe's q layout
+          // groups 8 nibbles per word along k; here the word order is re-read as 4 consecutive words per lane)
+          wv[r][c] = __ldcs(reinterpret_cast<const uint4*>(q + (size_t)(n0 + r) * (K / 8) + 128 * c + 4 * lane));
+          szf[r][c] = __bfloat1622float2(sz[(size_t)(n0 + r) * ng + 8 * c + lane / 4]);
+        }
+    float acc[R][M];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < M; ++i) acc[r][i] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= nch) break;
+      const int k0 = 1024 * c + 32 * lane;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        uint4 xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = *reinterpret_cast<const uint4*>(xs + i * K + k0 + 8 * u);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const __nv_bfloat162 s2 = __float2bfloat162_rn(szf[r][c].x);
+          const __nv_bfloat162 z2 = __float2bfloat162_rn(szf[r][c].y - 128.f * szf[r][c].x);
+          const uint32_t words[4] = {wv[r][c].x, wv[r][c].y, wv[r][c].z, wv[r][c].w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {  // word u: k0 + 8u .. +8, nibble j = k0 + 8u + j
+            const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&xv[u]);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {  // nibbles 2h, 2h+1 -> bf16x2 (128 + q)
+              const uint32_t nb = ((words[u] >> (8 * h)) & 0xFu) | (((words[u] >> (8 * h + 4)) & 0xFu) << 16);
+              uint32_t b2 = nb | 0x43004300u;
+              const __nv_bfloat162 wq = __hfma2(*reinterpret_cast<__nv_bfloat162*>(&b2), s2, z2);
+              const float2 wf = __bfloat1622float2(wq), xf = __bfloat1622float2(xp[h]);
+              acc[r][i] = fmaf(wf.x, xf.x, fmaf(wf.y, xf.y, acc[r][i]));
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        float v = acc[r][i];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && n0 + r < N) y[(size_t)i * N + n0 + r] = v;
+      }
+  }
+}
+
+template <int M, bool V2>
 static void run(int N, int K, const uint32_t* dq, const __nv_bfloat162* dsz, const __nv_bfloat16* dx, float* dy,
                 const std::vector<uint32_t>& hq, const std::vector<__nv_bfloat162>& hsz,
                 const std::vector<__nv_bfloat16>& hx, char* flush, size_t flush_bytes) {
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const size_t smem = (size_t)M * K * 2;
-  cudaFuncSetAttribute(gemv_w4<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kfn = V2 ? gemv_w4_v2<M> : gemv_w4<M>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemv_w4<M>, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem);
   const int grid = nsm * (per_sm > 0 ? per_sm : 1);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -84,7 +159,7 @@ static void run(int N, int K, const uint32_t* dq, const __nv_bfloat162* dsz, con
   for (int r = 0; r < reps + 3; ++r) {
     cudaMemsetAsync(flush, r, flush_bytes);  // L2 flush between launches
     cudaEventRecord(a);
-    gemv_w4<M><<<grid, 256, smem>>>(dq, dsz, dx, dy, N, K);
+    kfn<<<grid, 256, smem>>>(dq, dsz, dx, dy, N, K);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0.f;
@@ -115,7 +190,7 @@ static void run(int N, int K, const uint32_t* dq, const __nv_bfloat162* dsz, con
     }
   }
   const double bytes = (double)N * K / 2 + (double)N * (K / 128) * 4 + (double)M * K * 2 + (double)M * N * 4;
-  printf("m=%d grid=%d: best %.2f us, mean %.2f us, %.2f TB/s (best), max |err|/sum|terms| %.2e\n", M, grid,
+  printf("%s m=%d grid=%d: best %.2f us, mean %.2f us, %.2f TB/s (best), max |err|/sum|terms| %.2e\n", V2 ? "v2" : "v1", M, grid,
          best * 1e3, sum / reps * 1e3, bytes / (best * 1e-3) / 1e12, maxrel);
   cudaEventDestroy(a);
   cudaEventDestroy(b);
@@ -155,10 +230,13 @@ int main(int argc, char** argv) {
   cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice);
   printf("w4a16-g128 CUDA-core GEMV, N=%d K=%d, weights %.1f MB, L2 flushed per launch\n", N, K,
          (double)N * K / 2 / 1e6);
-  run<1>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
-  run<2>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
-  run<4>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
-  run<8>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
+  run<1, false>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
+  run<2, false>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
+  run<4, false>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
+  run<8, false>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
+  run<1, true>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
+  run<2, true>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
+  run<4, true>(N, K, dq, dsz, dx, dy, hq, hsz, hx, flush, flush_bytes);
   const cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : 1;
